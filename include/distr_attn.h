@@ -1,0 +1,120 @@
+/*
+ * distr_attn.h — C-ABI boundary of the B200 (sm_100a) DistrAttention forward hot path.
+ *
+ * DistrAttention (arXiv 2507.17245, /root/reference/PAPER.md "P:<line>"): for every query block
+ * of block_l rows, the d columns of Q are hashed with a 16-bit sign-random-projection LSH over the
+ * block's rows and Gray-ranked, stably sorted into groups of G* (Fig. 5), one
+ * representative Q column per group is sampled and the group's K columns are sum-fused (P:288,
+ * Eq. 2), and the reduced-d scores feed a blocked online-softmax attention with a
+ * full-d PV (Fig. 3). Readings of ambiguous passages: DESIGN.md §3.
+ *
+ * Conventions for every entry point below
+ *   - Tensor pointers are DEVICE pointers on the current CUDA device unless the name says host.
+ *     Q and O are [B, H, N, d] contiguous; K and V are [B, H_kv, N, d] contiguous
+ *     (H % H_kv == 0; query head h reads KV head h / (H / H_kv)). Element type = params.dtype
+ *     (DA_BF16: bfloat16, DA_F32: float; fp32 inputs are hashed in fp32 and rounded to bf16
+ *     for the tensor-core contractions, output written in fp32).
+ *   - The caller owns q, k, v, out, lse and the export buffers; the library owns its projection
+ *     cache and (when workspace == NULL) a grow-only device workspace pool per device.
+ *   - Calls are stream-ordered and asynchronous (`cuda_stream` is a cudaStream_t, NULL = legacy
+ *     default stream); synchronisation is the caller's job. Nothing throws across the ABI.
+ *   - Every argument is validated before anything is enqueued. On DA_ERR_INVALID /
+ *     DA_ERR_PRECONDITION nothing was enqueued and `out` is untouched. DA_ERR_CUDA means a CUDA
+ *     call failed (detail in distr_attn_last_error()); `out` is then unspecified.
+ *   - Thread safety: the projection cache and workspace pool are mutex-protected; concurrent
+ *     calls that share a library-managed workspace on one device must use one stream.
+ *
+ * Supported envelope: d in {64, 128}; block_l in {64, 128}; G* (group_size) in {1, 2, 4} with
+ * d % G* == 0 and the reduced width (128 / block_l) * d / G* in [16, 128]; any N >= 1 (ragged
+ * tails handled); any B, H >= 1 with B*H, B*H_kv < 65536.
+ */
+#ifndef DISTR_ATTN_H
+#define DISTR_ATTN_H
+
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes (mirroring the SPEC CLI convention S:537: 1 usage, 2 precondition, 3 runtime). */
+enum {
+  DA_OK = 0,
+  DA_ERR_INVALID = 1,      /* null pointer, non-positive dims, H % H_kv != 0, bad dtype flag */
+  DA_ERR_PRECONDITION = 2, /* d % G* != 0, reduced width < 16, unsupported
+                              d / block_l / G*, workspace too small */
+  DA_ERR_CUDA = 3          /* a CUDA runtime/driver call failed */
+};
+
+enum { DA_BF16 = 0, DA_F32 = 1 };
+
+typedef struct da_params {
+  int B, H, H_kv, N, d;        /* shapes, see above */
+  int block_l;                 /* Q-block height l: hashing block AND outer-loop block */
+  int group_size;              /* G*: constant group size */
+  unsigned long long seed;     /* projection-matrix seed ("randomly generated in prior") */
+  int causal;                  /* 0/1: query i attends keys 0..i (N_q == N_k); mask applied
+                                  after the approximation (reading R11) */
+  float scale;                 /* score scale; <= 0 selects 1/sqrt(d) with the ORIGINAL d (R12) */
+  int dtype;                   /* DA_BF16 | DA_F32 (inputs and output) */
+  void* workspace;             /* optional caller-owned device workspace; NULL = library pool */
+  size_t workspace_bytes;      /* size of `workspace` (>= distr_attn_workspace_size()) */
+  float* lse;                  /* optional [B, H, N] fp32 natural-log sum-exp of scaled scores */
+  unsigned short* bucket_ids;  /* optional [B, H, ceil(N/l), d] uint16 LSH bucket ids (tests) */
+  unsigned char* perm;         /* optional [B, H, ceil(N/l), d] uint8 stable sort permutation */
+} da_params;
+
+/* Fill `p` with defaults: H_kv = H, non-causal, bf16, scale = 1/sqrt(d), library workspace,
+ * no exports. Returns DA_OK, or DA_ERR_INVALID if p is NULL. */
+int distr_attn_init_params(da_params* p, int B, int H, int N, int d, int block_l, int group_size,
+                           unsigned long long seed);
+
+/* North-star entry point (BASELINE.json): DistrAttention forward with H_kv = H, non-causal,
+ * bf16, scale 1/sqrt(d), legacy default stream, library-managed workspace. */
+int distr_attn_fwd(const void* q, const void* k, const void* v, void* out, int B, int H, int N,
+                   int d, int block_l, int group_size, unsigned long long seed);
+
+/* DistrAttention forward, all options. Launches the LSH/prep kernel (hash -> Gray rank -> stable
+ * sort -> sampled Q̂, K^T layout pass) and the fused tcgen05 attention kernel (fusion of K
+ * columns per Q block, reduced-d QK^T, online softmax, full-d PV) on `cuda_stream`. */
+int distr_attn_fwd_ex(const void* q, const void* k, const void* v, void* out, const da_params* p,
+                      void* cuda_stream);
+
+/* Same as distr_attn_fwd_ex, but q/k/v/out (and lse/bucket_ids/perm if set) are HOST pointers:
+ * the call copies inputs to a library-owned device staging area, runs the forward and copies the
+ * result back, all on `cuda_stream`, and returns after the stream has synchronised. Host buffers
+ * should be pinned (cudaHostAlloc / torch pin_memory) for asynchronous copies. */
+int distr_attn_fwd_host(const void* q, const void* k, const void* v, void* out,
+                        const da_params* p, void* cuda_stream);
+
+/* Exact softmax attention (§2.1) on the same sm_100a tiling (G* ignored, no prep for
+ * bf16 inputs): the reference point for the speed-up. */
+int exact_attn_fwd_ex(const void* q, const void* k, const void* v, void* out, const da_params* p,
+                      void* cuda_stream);
+
+/* Run only the LSH step of the prep kernel and export p->bucket_ids and/or p->perm (at least one
+ * must be non-NULL). Bit-exact contract with the CPU oracle (fp32 fma chain, ascending rows). */
+int distr_attn_hash(const void* q, const da_params* p, void* cuda_stream);
+
+/* Host-side copy of the projection matrix for (seed, block_l): host_out = float[16 * block_l],
+ * row-major [k][r]. SplitMix64 counter stream + Box-Muller in double rounded to fp32 (R4). */
+int distr_attn_projection(unsigned long long seed, int block_l, float* host_out);
+
+/* Device workspace bytes needed by distr_attn_fwd_ex / exact_attn_fwd_ex for these params
+ * (0 if the params are invalid). */
+size_t distr_attn_workspace_size(const da_params* p);
+
+/* Static description of a status code. */
+const char* distr_attn_status_string(int status);
+
+/* Thread-local detail of the last error raised on the calling thread ("" if none). */
+const char* distr_attn_last_error(void);
+
+/* Number of kernel launches the last successful forward call on this thread enqueued. */
+int distr_attn_last_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* DISTR_ATTN_H */

@@ -1,0 +1,142 @@
+"""DistrAttention (arXiv 2507.17245) forward hot path, B200-native (sm_100a).
+
+Thin Python binding over the C-ABI in include/distr_attn.h: the functions below have the same
+names as the C entry points and only marshal torch tensors (device memory + current stream) into
+the da_params struct. Every compute step runs in libdistr_attn.so's CUDA kernels; there is no CPU
+or PyTorch fallback (a missing library raises).
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+
+import numpy as np
+import torch
+
+from . import _native
+from ._native import DA_BF16, DA_F32, DaParams, DistrAttnError, check, last_launch_count
+
+__all__ = [
+    "distr_attn_fwd", "distr_attn_fwd_ex", "exact_attn_fwd_ex", "distr_attn_fwd_host",
+    "distr_attn_hash", "distr_attn_projection", "distr_attn_workspace_size", "make_params",
+    "DistrAttnError", "last_launch_count",
+]
+
+_DT = {torch.bfloat16: DA_BF16, torch.float32: DA_F32}
+
+
+def _ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def make_params(q: torch.Tensor, k: torch.Tensor, *, block_l: int, group_size: int, seed: int = 0,
+                causal: bool = False, scale: float = 0.0, lse=None, bucket_ids=None, perm=None,
+                workspace=None) -> DaParams:
+    if q.dim() != 4 or k.dim() != 4:
+        raise ValueError("q must be [B,H,N,d] and k/v [B,H_kv,N,d]")
+    if q.dtype not in _DT:
+        raise ValueError(f"unsupported dtype {q.dtype}")
+    B, H, N, d = q.shape
+    p = DaParams()
+    p.B, p.H, p.H_kv, p.N, p.d = B, H, k.shape[1], N, d
+    p.block_l, p.group_size, p.seed = block_l, group_size, seed
+    p.causal, p.scale, p.dtype = int(bool(causal)), float(scale), _DT[q.dtype]
+    if workspace is not None:
+        p.workspace, p.workspace_bytes = workspace.data_ptr(), workspace.numel() * workspace.element_size()
+    p.lse = None if lse is None else lse.data_ptr()
+    p.bucket_ids = None if bucket_ids is None else bucket_ids.data_ptr()
+    p.perm = None if perm is None else perm.data_ptr()
+    return p
+
+
+def _check_tensors(*ts):
+    for t in ts:
+        if t is not None and not t.is_contiguous():
+            raise ValueError("tensors must be contiguous")
+
+
+def _stream(stream):
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return ctypes.c_void_p(stream.cuda_stream)
+
+
+def distr_attn_fwd_ex(q, k, v, out=None, *, block_l=128, group_size=2, seed=0, causal=False,
+                      scale=0.0, lse=None, bucket_ids=None, perm=None, workspace=None, stream=None):
+    """DistrAttention forward (device tensors, current torch stream). Returns `out`."""
+    _check_tensors(q, k, v, out, lse)
+    if out is None:
+        out = torch.empty_like(q)
+    p = make_params(q, k, block_l=block_l, group_size=group_size, seed=seed, causal=causal,
+                    scale=scale, lse=lse, bucket_ids=bucket_ids, perm=perm, workspace=workspace)
+    check(_native.lib().distr_attn_fwd_ex(_ptr(q), _ptr(k), _ptr(v), _ptr(out), ctypes.byref(p),
+                                          _stream(stream)))
+    return out
+
+
+def exact_attn_fwd_ex(q, k, v, out=None, *, block_l=128, causal=False, scale=0.0, lse=None,
+                      workspace=None, stream=None):
+    """Exact attention on the same sm_100a tiling (reference point). Returns `out`."""
+    _check_tensors(q, k, v, out, lse)
+    if out is None:
+        out = torch.empty_like(q)
+    p = make_params(q, k, block_l=block_l, group_size=1, causal=causal, scale=scale, lse=lse,
+                    workspace=workspace)
+    check(_native.lib().exact_attn_fwd_ex(_ptr(q), _ptr(k), _ptr(v), _ptr(out), ctypes.byref(p),
+                                          _stream(stream)))
+    return out
+
+
+def distr_attn_fwd(q, k, v, out, B, H, N, d, block_l, group_size, seed):
+    """North-star signature (legacy default stream, bf16, H_kv = H, non-causal)."""
+    check(_native.lib().distr_attn_fwd(_ptr(q), _ptr(k), _ptr(v), _ptr(out), B, H, N, d, block_l,
+                                       group_size, seed))
+    return out
+
+
+def distr_attn_fwd_host(q, k, v, out=None, *, block_l=128, group_size=2, seed=0, causal=False,
+                        scale=0.0, lse=None, stream=None):
+    """Forward over HOST (ideally pinned) tensors: H2D + kernels + D2H inside the C call."""
+    for t in (q, k, v):
+        if t.is_cuda:
+            raise ValueError("distr_attn_fwd_host takes host tensors")
+    _check_tensors(q, k, v, out, lse)
+    if out is None:
+        out = torch.empty_like(q)
+    p = make_params(q, k, block_l=block_l, group_size=group_size, seed=seed, causal=causal,
+                    scale=scale, lse=lse)
+    check(_native.lib().distr_attn_fwd_host(_ptr(q), _ptr(k), _ptr(v), _ptr(out), ctypes.byref(p),
+                                            _stream(stream)))
+    return out
+
+
+def distr_attn_hash(q, *, block_l=128, group_size=2, seed=0, stream=None):
+    """LSH step only: returns (bucket_ids uint16-as-int16 [B,H,nqb,d], perm uint8 [B,H,nqb,d])."""
+    _check_tensors(q)
+    B, H, N, d = q.shape
+    nqb = -(-N // block_l)
+    buckets = torch.empty((B, H, nqb, d), dtype=torch.int16, device=q.device)
+    perm = torch.empty((B, H, nqb, d), dtype=torch.uint8, device=q.device)
+    p = make_params(q, q, block_l=block_l, group_size=group_size, seed=seed, bucket_ids=buckets,
+                    perm=perm)
+    check(_native.lib().distr_attn_hash(_ptr(q), ctypes.byref(p), _stream(stream)))
+    return buckets, perm
+
+
+def distr_attn_projection(seed: int, block_l: int) -> np.ndarray:
+    out = np.empty((16, block_l), dtype=np.float32)
+    check(_native.lib().distr_attn_projection(seed, block_l, out.ctypes.data_as(ctypes.c_void_p)))
+    return out
+
+
+def distr_attn_workspace_size(q_shape, kv_heads, *, block_l=128, group_size=2,
+                              dtype=torch.bfloat16) -> int:
+    B, H, N, d = q_shape
+    p = DaParams()
+    p.B, p.H, p.H_kv, p.N, p.d = B, H, kv_heads, N, d
+    p.block_l, p.group_size, p.dtype = block_l, group_size, _DT[dtype]
+    return int(_native.lib().distr_attn_workspace_size(ctypes.byref(p)))
+
+
+def default_scale(d: int) -> float:
+    return 1.0 / math.sqrt(d)

@@ -1,0 +1,443 @@
+// api.cu — the C-ABI declared in include/distr_attn.h: validation, projection matrix, workspace,
+// TMA descriptors and launches. Host code only; kernels live in prep.cu / attn.cu.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "../../include/distr_attn.h"
+#include "../../include/distr_attn_profile.h"
+#include "internal.h"
+
+namespace {
+
+thread_local std::string g_last_error;
+thread_local int g_last_launches = 0;
+thread_local cudaEvent_t g_ev[3] = {nullptr, nullptr, nullptr};
+
+void record_ev(int i, cudaStream_t st) {
+  if (g_ev[i]) cudaEventRecord(g_ev[i], st);
+}
+
+int fail(int status, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return status;
+}
+
+#define DA_CUDA(expr)                                                                               \
+  do {                                                                                              \
+    cudaError_t e_ = (expr);                                                                        \
+    if (e_ != cudaSuccess)                                                                          \
+      return fail(DA_ERR_CUDA, "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(e_), __FILE__, __LINE__); \
+  } while (0)
+
+// ---------------------------------------------------------------------------- projection (R4)
+// SplitMix64 counter stream: n-th draw = mix(seed + (n + 1) * 0x9E3779B97F4A7C15); uniform in
+// (0,1) from the top 53 bits + 0.5; Box-Muller on consecutive pairs in double; rounded to fp32;
+// entries row-major [k][r]. (Independent implementation of the same generator as the oracle.)
+inline uint64_t sm64_mix(uint64_t x) {
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ULL;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBULL;
+  return x ^ (x >> 31);
+}
+void make_projection(uint64_t seed, int block_l, float* out) {
+  const uint64_t gamma = 0x9E3779B97F4A7C15ULL;
+  const int n = 16 * block_l;
+  uint64_t ctr = seed;
+  for (int e = 0; e < n; e += 2) {
+    ctr += gamma;
+    const double u1 = (double)(sm64_mix(ctr) >> 11) * 0x1.0p-53 + 0x1.0p-54;
+    ctr += gamma;
+    const double u2 = (double)(sm64_mix(ctr) >> 11) * 0x1.0p-53 + 0x1.0p-54;
+    const double rad = std::sqrt(-2.0 * std::log(u1));
+    const double ang = 6.283185307179586476925286766559 * u2;
+    out[e] = (float)(rad * std::cos(ang));
+    out[e + 1] = (float)(rad * std::sin(ang));
+  }
+}
+
+std::mutex g_mu;
+std::map<std::tuple<int, uint64_t, int>, float*> g_proj;  // (device, seed, block_l) -> device ptr
+struct Pool {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+};
+std::map<int, Pool> g_pool;       // per-device workspace
+std::map<int, Pool> g_host_pool;  // per-device staging for distr_attn_fwd_host
+
+int get_projection(int dev, uint64_t seed, int block_l, cudaStream_t st, const float** out) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto key = std::make_tuple(dev, seed, block_l);
+  auto it = g_proj.find(key);
+  if (it != g_proj.end()) {
+    *out = it->second;
+    return DA_OK;
+  }
+  std::vector<float> h(16 * block_l);
+  make_projection(seed, block_l, h.data());
+  float* d = nullptr;
+  DA_CUDA(cudaMalloc(&d, h.size() * sizeof(float)));
+  // Synchronous copy on first use of (seed, block_l) only; never on the steady-state path.
+  DA_CUDA(cudaMemcpy(d, h.data(), h.size() * sizeof(float), cudaMemcpyHostToDevice));
+  (void)st;
+  g_proj[key] = d;
+  *out = d;
+  return DA_OK;
+}
+
+int get_pool(std::map<int, Pool>& pools, int dev, size_t need, void** out) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  Pool& p = pools[dev];
+  if (p.bytes < need) {
+    if (p.ptr) {
+      DA_CUDA(cudaDeviceSynchronize());
+      DA_CUDA(cudaFree(p.ptr));
+      p.ptr = nullptr;
+      p.bytes = 0;
+    }
+    DA_CUDA(cudaMalloc(&p.ptr, need));
+    p.bytes = need;
+  }
+  *out = p.ptr;
+  return DA_OK;
+}
+
+// ---------------------------------------------------------------------------- plan
+struct Plan {
+  int B, H, Hkv, N, d, l, G, HB, DR, nqb, nqt, nkt, N_pad, f32, causal;
+  float scale;
+  size_t off_perm, off_qhat, off_kt, off_qc, off_kc, off_vc, total;
+};
+
+inline size_t al256(size_t x) { return (x + 255) / 256 * 256; }
+
+int validate(const da_params* p, bool distr, Plan* P) {
+  if (!p) return fail(DA_ERR_INVALID, "params is NULL");
+  if (p->B <= 0 || p->H <= 0 || p->H_kv <= 0 || p->N <= 0 || p->d <= 0 || p->block_l <= 0)
+    return fail(DA_ERR_INVALID, "non-positive dimension (B=%d H=%d H_kv=%d N=%d d=%d block_l=%d)", p->B, p->H,
+                p->H_kv, p->N, p->d, p->block_l);
+  if (p->H % p->H_kv) return fail(DA_ERR_INVALID, "H (%d) not a multiple of H_kv (%d)", p->H, p->H_kv);
+  if (p->dtype != DA_BF16 && p->dtype != DA_F32) return fail(DA_ERR_INVALID, "dtype %d", p->dtype);
+  if (p->causal != 0 && p->causal != 1) return fail(DA_ERR_INVALID, "causal must be 0/1");
+  if ((long long)p->B * p->H >= 65536 || (long long)p->B * p->H_kv >= 65536)
+    return fail(DA_ERR_INVALID, "B*H too large");
+  if (p->d != 64 && p->d != 128) return fail(DA_ERR_PRECONDITION, "d=%d unsupported (64|128)", p->d);
+  if (p->block_l != 64 && p->block_l != 128)
+    return fail(DA_ERR_PRECONDITION, "block_l=%d unsupported (64|128)", p->block_l);
+  const int G = distr ? p->group_size : 1;
+  if (distr) {
+    if (G <= 0) return fail(DA_ERR_INVALID, "group_size=%d", G);
+    if (p->d % G) return fail(DA_ERR_PRECONDITION, "d %% G* != 0 (d=%d, G*=%d)", p->d, G);
+    if (G != 1 && G != 2 && G != 4) return fail(DA_ERR_PRECONDITION, "G*=%d unsupported (1|2|4)", G);
+    if (p->d / G < 16) return fail(DA_ERR_PRECONDITION, "d/G* = %d < 16", p->d / G);
+  }
+  Plan& q = *P;
+  q.B = p->B; q.H = p->H; q.Hkv = p->H_kv; q.N = p->N; q.d = p->d; q.l = p->block_l; q.G = G;
+  q.HB = 128 / p->block_l;
+  q.DR = q.HB * q.d / G;
+  if (distr && (q.DR > 128 || q.DR < 16))
+    return fail(DA_ERR_PRECONDITION, "reduced width (128/block_l)*d/G* = %d outside [16,128]", q.DR);
+  q.nqb = (q.N + q.l - 1) / q.l;
+  q.nqt = (q.N + 127) / 128;
+  q.nkt = (q.N + 127) / 128;
+  q.N_pad = (q.N + 7) / 8 * 8;
+  q.f32 = p->dtype == DA_F32;
+  q.causal = p->causal;
+  q.scale = p->scale > 0.f ? p->scale : (float)(1.0 / std::sqrt((double)q.d));
+  const size_t BH = (size_t)q.B * q.H, BHkv = (size_t)q.B * q.Hkv;
+  size_t o = 0;
+  q.off_perm = q.off_qhat = q.off_kt = q.off_qc = q.off_kc = q.off_vc = 0;
+  if (distr) {
+    q.off_perm = o; o = al256(o + BH * q.nqb * q.d);
+    q.off_qhat = o; o = al256(o + BH * q.N * q.DR * 2);
+    q.off_kt = o;   o = al256(o + BHkv * q.d * q.N_pad * 2);
+  } else if (q.f32) {
+    q.off_qc = o; o = al256(o + BH * q.N * q.d * 2);
+    q.off_kc = o; o = al256(o + BHkv * q.N * q.d * 2);
+  }
+  if (q.f32) { q.off_vc = o; o = al256(o + BHkv * q.N * q.d * 2); }
+  q.total = o;
+  return DA_OK;
+}
+
+// ---------------------------------------------------------------------------- TMA descriptors
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+int get_encode(EncodeTiledFn* fn) {
+  static EncodeTiledFn cached = nullptr;
+  static std::once_flag once;
+  static cudaError_t err = cudaSuccess;
+  std::call_once(once, [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    err = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q);
+    if (err == cudaSuccess && q == cudaDriverEntryPointSuccess) cached = reinterpret_cast<EncodeTiledFn>(f);
+  });
+  if (!cached) return fail(DA_ERR_CUDA, "cuTensorMapEncodeTiled unavailable (%s)", cudaGetErrorString(err));
+  *fn = cached;
+  return DA_OK;
+}
+
+// 3-D bf16 tensor [d2][d1][d0] (d0 innermost), box {b0, b1, 1}.
+int make_map(CUtensorMap* m, const void* base, uint64_t d0, uint64_t d1, uint64_t d2, uint32_t b0, uint32_t b1,
+             int swizzle_bytes) {
+  EncodeTiledFn enc;
+  if (int s = get_encode(&enc)) return s;
+  cuuint64_t dims[3] = {d0, d1, d2};
+  cuuint64_t strides[2] = {d0 * 2, d0 * d1 * 2};
+  cuuint32_t box[3] = {b0, b1, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUtensorMapSwizzle sw = swizzle_bytes == 128  ? CU_TENSOR_MAP_SWIZZLE_128B
+                          : swizzle_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                          : swizzle_bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
+                                                : CU_TENSOR_MAP_SWIZZLE_NONE;
+  CUresult r = enc(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 3, const_cast<void*>(base), dims, strides, box, es,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS)
+    return fail(DA_ERR_CUDA, "cuTensorMapEncodeTiled failed (%d) dims=[%llu,%llu,%llu] box=[%u,%u]", (int)r,
+                (unsigned long long)d0, (unsigned long long)d1, (unsigned long long)d2, b0, b1);
+  return DA_OK;
+}
+
+int current_device(int* dev) {
+  DA_CUDA(cudaGetDevice(dev));
+  return DA_OK;
+}
+
+// ---------------------------------------------------------------------------- forward
+int forward(const void* q, const void* k, const void* v, void* out, const da_params* p, cudaStream_t st,
+            bool distr) {
+  Plan P;
+  if (int s = validate(p, distr, &P)) return s;
+  if (!q || !k || !v || !out) return fail(DA_ERR_INVALID, "null tensor pointer");
+  int dev;
+  if (int s = current_device(&dev)) return s;
+  uint8_t* ws = nullptr;
+  if (P.total) {
+    if (p->workspace) {
+      if (p->workspace_bytes < P.total)
+        return fail(DA_ERR_PRECONDITION, "workspace too small (%zu < %zu)", p->workspace_bytes, P.total);
+      ws = static_cast<uint8_t*>(p->workspace);
+    } else {
+      void* w;
+      if (int s = get_pool(g_pool, dev, P.total, &w)) return s;
+      ws = static_cast<uint8_t*>(w);
+    }
+  }
+  const float* proj = nullptr;
+  if (distr)
+    if (int s = get_projection(dev, p->seed, P.l, st, &proj)) return s;
+
+  const size_t BH = (size_t)P.B * P.H, BHkv = (size_t)P.B * P.Hkv;
+  int launches = 0;
+  record_ev(0, st);
+  const void* kv_v = v;
+  if (P.f32) {
+    uint16_t* vc = reinterpret_cast<uint16_t*>(ws + P.off_vc);
+    DA_CUDA(da::launch_convert_bf16(static_cast<const float*>(v), vc, BHkv * P.N * P.d, st));
+    ++launches;
+    kv_v = vc;
+  }
+  const void* a_src;
+  const void* k_src;
+  if (distr) {
+    da::PrepArgs a{};
+    a.q = q; a.k = k; a.in_f32 = P.f32;
+    a.BH = (int)BH; a.BHkv = (int)BHkv; a.N = P.N; a.d = P.d; a.block_l = P.l; a.G = P.G; a.HB = P.HB;
+    a.DR = P.DR; a.nqb = P.nqb; a.N_pad = P.N_pad; a.proj = proj;
+    a.perm_ws = ws + P.off_perm;
+    a.bucket_out = p->bucket_ids;
+    a.perm_out = p->perm;
+    a.qhat = reinterpret_cast<uint16_t*>(ws + P.off_qhat);
+    a.kt = reinterpret_cast<uint16_t*>(ws + P.off_kt);
+    a.n_hash_ctas = (int)(BH * P.nqb);
+    a.n_kt_ctas = (int)(BHkv * ((P.N + 63) / 64));
+    DA_CUDA(da::launch_prep(a, st));
+    ++launches;
+    a_src = a.qhat;
+    k_src = a.kt;
+  } else if (P.f32) {
+    uint16_t* qc = reinterpret_cast<uint16_t*>(ws + P.off_qc);
+    uint16_t* kc = reinterpret_cast<uint16_t*>(ws + P.off_kc);
+    DA_CUDA(da::launch_convert_bf16(static_cast<const float*>(q), qc, BH * P.N * P.d, st));
+    DA_CUDA(da::launch_convert_bf16(static_cast<const float*>(k), kc, BHkv * P.N * P.d, st));
+    launches += 2;
+    a_src = qc;
+    k_src = kc;
+  } else {
+    a_src = q;
+    k_src = k;
+  }
+
+  CUtensorMap tmA, tmK, tmV;
+  if (distr) {
+    const int sw = P.DR * 2 >= 128 ? 128 : P.DR * 2;
+    if (int s = make_map(&tmA, a_src, P.DR, P.N, BH, sw / 2, 128, sw)) return s;
+    if (int s = make_map(&tmK, k_src, P.N_pad, P.d, BHkv, 128, P.d, 0)) return s;
+  } else {
+    if (int s = make_map(&tmA, a_src, P.d, P.N, BH, 64, 128, 128)) return s;
+    if (int s = make_map(&tmK, k_src, P.d, P.N, BHkv, 64, 128, 128)) return s;
+  }
+  if (int s = make_map(&tmV, kv_v, P.d, P.N, BHkv, 64, 128, 128)) return s;
+
+  da::AttnArgs aa{};
+  aa.N = P.N; aa.H = P.H; aa.H_kv = P.Hkv; aa.nqt = P.nqt; aa.nkt = P.nkt; aa.nqb = P.nqb; aa.block_l = P.l;
+  aa.scale_log2 = P.scale * 1.4426950408889634f;
+  aa.causal = P.causal;
+  aa.perm = distr ? ws + P.off_perm : nullptr;
+  aa.out = out;
+  aa.out_f32 = P.f32;
+  aa.lse = p->lse;
+  da::AttnLaunch L{P.d, P.G, P.HB, distr ? 1 : 0, (int)BH, &tmA, &tmK, &tmV};
+  record_ev(1, st);
+  DA_CUDA(da::launch_attn(L, aa, st));
+  record_ev(2, st);
+  g_ev[0] = g_ev[1] = g_ev[2] = nullptr;
+  ++launches;
+  g_last_launches = launches;
+  return DA_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int distr_attn_init_params(da_params* p, int B, int H, int N, int d, int block_l, int group_size,
+                           unsigned long long seed) {
+  if (!p) return fail(DA_ERR_INVALID, "params is NULL");
+  std::memset(p, 0, sizeof(*p));
+  p->B = B; p->H = H; p->H_kv = H; p->N = N; p->d = d; p->block_l = block_l; p->group_size = group_size;
+  p->seed = seed;
+  p->causal = 0;
+  p->scale = 0.f;
+  p->dtype = DA_BF16;
+  return DA_OK;
+}
+
+int distr_attn_fwd(const void* q, const void* k, const void* v, void* out, int B, int H, int N, int d,
+                   int block_l, int group_size, unsigned long long seed) {
+  da_params p;
+  distr_attn_init_params(&p, B, H, N, d, block_l, group_size, seed);
+  return forward(q, k, v, out, &p, nullptr, true);
+}
+
+int distr_attn_fwd_ex(const void* q, const void* k, const void* v, void* out, const da_params* p,
+                      void* cuda_stream) {
+  return forward(q, k, v, out, p, static_cast<cudaStream_t>(cuda_stream), true);
+}
+
+int exact_attn_fwd_ex(const void* q, const void* k, const void* v, void* out, const da_params* p,
+                      void* cuda_stream) {
+  return forward(q, k, v, out, p, static_cast<cudaStream_t>(cuda_stream), false);
+}
+
+int distr_attn_fwd_host(const void* q, const void* k, const void* v, void* out, const da_params* p,
+                        void* cuda_stream) {
+  Plan P;
+  if (int s = validate(p, true, &P)) return s;
+  if (!q || !k || !v || !out) return fail(DA_ERR_INVALID, "null tensor pointer");
+  cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+  const size_t es = P.f32 ? 4 : 2;
+  const size_t nq = (size_t)P.B * P.H * P.N * P.d * es, nkv = (size_t)P.B * P.Hkv * P.N * P.d * es;
+  const size_t nlse = p->lse ? (size_t)P.B * P.H * P.N * 4 : 0;
+  const size_t nexp = (size_t)P.B * P.H * P.nqb * P.d;
+  const size_t nb = p->bucket_ids ? nexp * 2 : 0, np = p->perm ? nexp : 0;
+  const size_t o_q = 0, o_k = al256(o_q + nq), o_v = al256(o_k + nkv), o_o = al256(o_v + nkv),
+               o_l = al256(o_o + nq), o_b = al256(o_l + nlse), o_p = al256(o_b + nb), tot = al256(o_p + np);
+  int dev;
+  if (int s = current_device(&dev)) return s;
+  void* stage;
+  if (int s = get_pool(g_host_pool, dev, tot, &stage)) return s;
+  uint8_t* S = static_cast<uint8_t*>(stage);
+  DA_CUDA(cudaMemcpyAsync(S + o_q, q, nq, cudaMemcpyHostToDevice, st));
+  DA_CUDA(cudaMemcpyAsync(S + o_k, k, nkv, cudaMemcpyHostToDevice, st));
+  DA_CUDA(cudaMemcpyAsync(S + o_v, v, nkv, cudaMemcpyHostToDevice, st));
+  da_params dp = *p;
+  dp.lse = p->lse ? reinterpret_cast<float*>(S + o_l) : nullptr;
+  dp.bucket_ids = p->bucket_ids ? reinterpret_cast<unsigned short*>(S + o_b) : nullptr;
+  dp.perm = p->perm ? S + o_p : nullptr;
+  if (int s = forward(S + o_q, S + o_k, S + o_v, S + o_o, &dp, st, true)) return s;
+  DA_CUDA(cudaMemcpyAsync(out, S + o_o, nq, cudaMemcpyDeviceToHost, st));
+  if (p->lse) DA_CUDA(cudaMemcpyAsync(p->lse, S + o_l, nlse, cudaMemcpyDeviceToHost, st));
+  if (p->bucket_ids) DA_CUDA(cudaMemcpyAsync(p->bucket_ids, S + o_b, nb, cudaMemcpyDeviceToHost, st));
+  if (p->perm) DA_CUDA(cudaMemcpyAsync(p->perm, S + o_p, np, cudaMemcpyDeviceToHost, st));
+  DA_CUDA(cudaStreamSynchronize(st));
+  return DA_OK;
+}
+
+int distr_attn_hash(const void* q, const da_params* p, void* cuda_stream) {
+  Plan P;
+  if (int s = validate(p, true, &P)) return s;
+  if (!q) return fail(DA_ERR_INVALID, "null q");
+  if (!p->bucket_ids && !p->perm) return fail(DA_ERR_INVALID, "no export buffer (bucket_ids / perm)");
+  cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
+  int dev;
+  if (int s = current_device(&dev)) return s;
+  const float* proj;
+  if (int s = get_projection(dev, p->seed, P.l, st, &proj)) return s;
+  da::PrepArgs a{};
+  a.q = q; a.k = nullptr; a.in_f32 = P.f32;
+  a.BH = P.B * P.H; a.BHkv = P.B * P.Hkv; a.N = P.N; a.d = P.d; a.block_l = P.l; a.G = P.G; a.HB = P.HB;
+  a.DR = P.DR; a.nqb = P.nqb; a.N_pad = P.N_pad; a.proj = proj;
+  a.bucket_out = p->bucket_ids;
+  a.perm_out = p->perm;
+  a.n_hash_ctas = P.B * P.H * P.nqb;
+  a.n_kt_ctas = 0;
+  DA_CUDA(da::launch_prep(a, st));
+  g_last_launches = 1;
+  return DA_OK;
+}
+
+int distr_attn_projection(unsigned long long seed, int block_l, float* host_out) {
+  if (!host_out) return fail(DA_ERR_INVALID, "host_out is NULL");
+  if (block_l <= 0) return fail(DA_ERR_INVALID, "block_l=%d", block_l);
+  make_projection(seed, block_l, host_out);
+  return DA_OK;
+}
+
+size_t distr_attn_workspace_size(const da_params* p) {
+  Plan P;
+  if (validate(p, true, &P)) return 0;
+  Plan E;
+  validate(p, false, &E);
+  return P.total > E.total ? P.total : E.total;
+}
+
+const char* distr_attn_status_string(int status) {
+  switch (status) {
+    case DA_OK: return "ok";
+    case DA_ERR_INVALID: return "invalid argument";
+    case DA_ERR_PRECONDITION: return "unsupported configuration / precondition violated";
+    case DA_ERR_CUDA: return "CUDA error";
+    default: return "unknown status";
+  }
+}
+
+const char* distr_attn_last_error(void) { return g_last_error.c_str(); }
+
+int distr_attn_last_launch_count(void) { return g_last_launches; }
+
+int distr_attn_set_profile_events(void* ev_start, void* ev_attn, void* ev_end) {
+  g_ev[0] = static_cast<cudaEvent_t>(ev_start);
+  g_ev[1] = static_cast<cudaEvent_t>(ev_attn);
+  g_ev[2] = static_cast<cudaEvent_t>(ev_end);
+  return DA_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,53 @@
+// internal.h — launcher interfaces shared by the host C-ABI (api.cu) and the kernel translation
+// units (prep.cu, attn.cu). Not part of the public ABI.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+namespace da {
+
+// Everything the prep (LSH) kernel needs. All pointers are device pointers.
+struct PrepArgs {
+  const void* q;       // [BH][N][d] (bf16 or f32)
+  const void* k;       // [BHkv][N][d]
+  int in_f32;          // input element type: 0 bf16, 1 f32
+  int BH, BHkv, N, d, block_l, G, HB, DR, nqb, N_pad;
+  const float* proj;   // [16][block_l]
+  uint8_t* perm_ws;    // [BH][nqb][d]  (nullable in hash-only mode)
+  uint16_t* bucket_out;  // optional export [BH][nqb][d]
+  uint8_t* perm_out;     // optional export [BH][nqb][d]
+  uint16_t* qhat;      // [BH][N][DR] bf16 bits (nullable: hash only)
+  uint16_t* kt;        // [BHkv][d][N_pad] bf16 bits (nullable)
+  int n_hash_ctas;     // BH * nqb (0 = no hashing)
+  int n_kt_ctas;       // BHkv * ceil(N/64) (0 = no K^T pass)
+};
+
+// Everything the attention kernel needs besides its three TMA descriptors.
+struct AttnArgs {
+  int N, H, H_kv, nqt, nkt, nqb, block_l;
+  float scale_log2;  // scale * log2(e)
+  int causal;
+  const uint8_t* perm;  // [BH][nqb][d] (distr only)
+  void* out;            // [BH][N][d]
+  int out_f32;
+  float* lse;           // optional [BH][N]
+};
+
+cudaError_t launch_prep(const PrepArgs& a, cudaStream_t st);
+cudaError_t launch_convert_bf16(const float* src, uint16_t* dst, size_t n, cudaStream_t st);
+
+// Which kernel flavour: DISTR with (d, G, HB) or exact with d.
+struct AttnLaunch {
+  int d, G, HB, distr;
+  int BH;
+  const CUtensorMap* tmA;  // Q (exact) or Q̂ (distr)
+  const CUtensorMap* tmK;  // K natural (exact) or K^T (distr)
+  const CUtensorMap* tmV;
+};
+cudaError_t launch_attn(const AttnLaunch& L, const AttnArgs& a, cudaStream_t st);
+// Shared memory bytes the attention kernel uses (0 if unsupported combination).
+size_t attn_smem_bytes(int d, int G, int HB, int distr);
+
+}  // namespace da

@@ -1,0 +1,209 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle on the same seeded inputs.
+
+Bar (north_star): LSH bucket ids and permutations bit-exact; outputs within max-abs 2e-2 and
+mean-abs 2e-3 of the oracle's DistrAttention (and of the exact oracle for the exact kernel).
+Large configs are checked on sampled Q blocks: each Q block is an independent unit of the method
+(§3.3), so the sampled comparison is exact for those blocks.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2507_17245_b200 as da
+from gpu_util import MAX_ABS, MEAN_ABS, errors, gather_items, oracle_items, to_np32, valid_rows_mask
+from synth import CONFIGS, Config, make_qkv, sample_items
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+
+
+def cfg_small(**kw):
+    base = dict(name="t", B=1, H=2, H_kv=2, N=256, d=64, block_l=64, group_size=2, causal=False,
+                dtype="bf16", data_seed=5)
+    base.update(kw)
+    return Config(**base)
+
+
+# ------------------------------------------------------------------------------ hashing
+def check_hash(cfg: Config, dist="normal", heads=None, scale_q=1.0, zero_cols=()):
+    q, _, _ = make_qkv(cfg, dist=dist, device=DEV)
+    if scale_q != 1.0:
+        q = q * scale_q
+    for c in zero_cols:
+        q[..., c] = 0
+    q = q.contiguous()
+    bk, pm = da.distr_attn_hash(q, block_l=cfg.block_l, group_size=cfg.group_size, seed=11)
+    torch.cuda.synchronize()
+    bk = bk.cpu().numpy().view(np.uint16)
+    pm = pm.cpu().numpy()
+    heads = heads or [(b, h) for b in range(cfg.B) for h in range(cfg.H)]
+    for b, h in heads:
+        ob, op = oracle.hash_all(to_np32(q[b:b + 1, h:h + 1]), cfg.block_l, 11)
+        assert np.array_equal(bk[b, h], ob[0, 0]), (b, h, np.argwhere(bk[b, h] != ob[0, 0])[:5])
+        assert np.array_equal(pm[b, h], op[0, 0]), (b, h)
+    return bk
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4", "C5"])
+def test_hash_bit_exact_all_configs(name):
+    cfg = CONFIGS[name]
+    if name == "C5":
+        cfg = cfg.with_(B=2)  # same per-head shape; full-batch hashing is covered by bench parity
+    heads = None if cfg.B * cfg.H <= 64 else [(0, 0), (cfg.B - 1, cfg.H - 1), (1, 3)]
+    if cfg.B * cfg.H > 64:
+        heads = [(b % cfg.B, h % cfg.H) for b, h in heads]
+    check_hash(cfg, heads=heads)
+
+
+@pytest.mark.parametrize("dist", ["uniform", "clustered"])
+def test_hash_stress_distributions(dist):
+    check_hash(cfg_small(N=197, d=64, block_l=64, H=3), dist=dist)
+    check_hash(cfg_small(N=300, d=128, block_l=128, H=2), dist=dist)
+
+
+def test_hash_zero_columns_and_pow2_scaling():
+    cfg = cfg_small(N=256, d=128, block_l=128)
+    a = check_hash(cfg, zero_cols=(0, 5, 77))
+    assert np.all(a[..., [0, 5, 77]] == 0)
+    b = check_hash(cfg, scale_q=2.0 ** -7, zero_cols=(0, 5, 77))
+    assert np.array_equal(a, b)
+
+
+def test_hash_fp32_input():
+    check_hash(CONFIGS["C1"])
+    check_hash(cfg_small(dtype="f32", N=333, d=128, block_l=128))
+
+
+# ------------------------------------------------------------------------------ attention
+def run_and_compare(cfg: Config, *, G=None, dist="normal", items=None, exact=False, seed=0,
+                    oracle_G=None, q=None, k=None, v=None):
+    G = cfg.group_size if G is None else G
+    if q is None:
+        q, k, v = make_qkv(cfg, dist=dist, device=DEV)
+    if exact:
+        out = da.exact_attn_fwd_ex(q, k, v, block_l=cfg.block_l, causal=cfg.causal)
+    else:
+        out = da.distr_attn_fwd_ex(q, k, v, block_l=cfg.block_l, group_size=G, seed=seed,
+                                   causal=cfg.causal)
+    torch.cuda.synchronize()
+    if items is None:
+        items = [(bh, qb) for bh in range(cfg.B * cfg.H) for qb in range(cfg.nqb)]
+    og = (0 if exact else G) if oracle_G is None else oracle_G
+    want = oracle_items(q, k, v, items, block_l=cfg.block_l, G=og, seed=seed, causal=cfg.causal)
+    got = gather_items(out, items, cfg.block_l)
+    mask = valid_rows_mask(items, cfg.N, cfg.block_l, cfg.d)
+    mx, mean = errors(got, want, mask)
+    assert np.isfinite(got[mask]).all()
+    return mx, mean, out
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4", "C5"])
+def test_distr_parity_configs(name):
+    cfg = CONFIGS[name]
+    if name == "C5":
+        cfg = cfg.with_(B=4)  # per-head shape of C5; the full B=32 job is sampled in bench
+    items = None if cfg.B * cfg.H * cfg.nqb <= 4096 else sample_items(cfg, n_heads=3, per_head=3)
+    mx, mean, _ = run_and_compare(cfg, items=items)
+    assert mx <= MAX_ABS and mean <= MEAN_ABS, (name, mx, mean)
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C4"])
+def test_exact_parity_configs(name):
+    cfg = CONFIGS[name]
+    items = None if cfg.B * cfg.H * cfg.nqb <= 4096 else sample_items(cfg, n_heads=3, per_head=3)
+    mx, mean, _ = run_and_compare(cfg, items=items, exact=True)
+    assert mx <= MAX_ABS and mean <= MEAN_ABS, (name, mx, mean)
+
+
+@pytest.mark.parametrize("d,block_l,G", [(64, 64, 1), (64, 64, 2), (64, 64, 4), (64, 128, 1),
+                                         (64, 128, 2), (64, 128, 4), (128, 128, 1),
+                                         (128, 128, 2), (128, 128, 4), (128, 64, 2),
+                                         (128, 64, 4)])
+@pytest.mark.parametrize("causal", [False, True])
+def test_distr_parity_envelope(d, block_l, G, causal):
+    # several Q/K tiles plus ragged tails, GQA (H=4 over H_kv=2)
+    cfg = cfg_small(B=2, H=4, H_kv=2, N=333, d=d, block_l=block_l, group_size=G, causal=causal)
+    mx, mean, _ = run_and_compare(cfg)
+    assert mx <= MAX_ABS and mean <= MEAN_ABS, (mx, mean)
+
+
+@pytest.mark.parametrize("N", [1, 2, 63, 64, 65, 127, 128, 129, 255, 256, 257, 640])
+@pytest.mark.parametrize("exact", [False, True])
+def test_ragged_lengths(N, exact):
+    cfg = cfg_small(N=N, d=128, block_l=128, H=2)
+    mx, mean, _ = run_and_compare(cfg, exact=exact)
+    assert mx <= MAX_ABS and mean <= MEAN_ABS, (N, mx, mean)
+
+
+def test_group_size_one_matches_exact_oracle():
+    cfg = cfg_small(N=300, d=128, block_l=128, group_size=1, causal=True)
+    mx, mean, _ = run_and_compare(cfg, oracle_G=0)
+    assert mx <= MAX_ABS and mean <= MEAN_ABS, (mx, mean)
+
+
+@pytest.mark.parametrize("G", [2, 4])
+def test_duplicated_columns_match_exact_oracle(G):
+    # Eq. 1: G identical copies per group -> DistrAttention == exact attention
+    cfg = cfg_small(N=384, d=128, block_l=128, group_size=G)
+    g = torch.Generator(device=DEV).manual_seed(3)
+    base = torch.randn((1, 2, 384, 128 // G), generator=g, device=DEV)
+    q = base.repeat_interleave(G, dim=-1).bfloat16().contiguous()
+    k = torch.randn((1, 2, 384, 128), generator=g, device=DEV).bfloat16()
+    v = torch.randn((1, 2, 384, 128), generator=g, device=DEV).bfloat16()
+    mx, mean, _ = run_and_compare(cfg, oracle_G=0, q=q, k=k, v=v)
+    assert mx <= MAX_ABS and mean <= MEAN_ABS, (mx, mean)
+
+
+def test_uniform_inputs_paper_distribution():
+    cfg = cfg_small(N=512, d=128, block_l=128, H=2)
+    mx, mean, _ = run_and_compare(cfg, dist="uniform")
+    assert mx <= MAX_ABS and mean <= MEAN_ABS, (mx, mean)
+
+
+def test_lse_and_host_entry_point():
+    cfg = cfg_small(N=300, d=128, block_l=128, H=2)
+    q, k, v = make_qkv(cfg, device=DEV)
+    lse = torch.empty((1, 2, 300), device=DEV)
+    out = da.distr_attn_fwd_ex(q, k, v, block_l=128, group_size=2, lse=lse)
+    torch.cuda.synchronize()
+    # host entry point: same result bit for bit (same kernels, same inputs)
+    oh = da.distr_attn_fwd_host(q.cpu().pin_memory(), k.cpu().pin_memory(), v.cpu().pin_memory(),
+                                block_l=128, group_size=2)
+    assert torch.equal(oh, out.cpu())
+    # lse against the oracle's Ŝ log-sum-exp (sampling of one Q block)
+    _, lse_ref = oracle.attn_items(to_np32(q), to_np32(k), to_np32(v), [(1, 2)], block_l=128, G=2,
+                                   want_lse=True)
+    got = lse[0, 1, 256:300].cpu().numpy()
+    np.testing.assert_allclose(got, lse_ref[0, :44], atol=2e-2)
+
+
+def test_north_star_entry_point_and_determinism():
+    cfg = cfg_small(N=1000, d=128, block_l=128, H=4)
+    q, k, v = make_qkv(cfg, device=DEV)
+    out = torch.empty_like(q)
+    torch.cuda.synchronize()
+    da.distr_attn_fwd(q, k, v, out, 1, 4, 1000, 128, 128, 2, 0)
+    torch.cuda.synchronize()
+    out2 = da.distr_attn_fwd_ex(q, k, v, block_l=128, group_size=2, seed=0)
+    torch.cuda.synchronize()
+    assert torch.equal(out, out2)
+    mx, mean, _ = run_and_compare(cfg, q=q, k=k, v=v)
+    assert mx <= MAX_ABS and mean <= MEAN_ABS
+
+
+def test_error_against_exact_is_reported_not_gated():
+    # on i.i.d. N(0,1) inputs DistrAttention differs from exact attention by
+    # ~0.6 max / ~0.07 mean at G*=2; the kernel must reproduce the oracle's approximation, i.e.
+    # its distance to the exact oracle must match the oracle's own distance.
+    cfg = cfg_small(N=256, d=64, block_l=64, H=2)
+    q, k, v = make_qkv(cfg, device=DEV)
+    out = da.distr_attn_fwd_ex(q, k, v, block_l=64, group_size=2)
+    torch.cuda.synchronize()
+    items = [(bh, qb) for bh in range(2) for qb in range(4)]
+    ex = oracle_items(q, k, v, items, block_l=64, G=0)
+    di = oracle_items(q, k, v, items, block_l=64, G=2)
+    got = gather_items(out, items, 64)
+    e_or = np.abs(di - ex).mean()
+    e_gpu = np.abs(got - ex).mean()
+    assert abs(e_gpu - e_or) < 0.1 * e_or
