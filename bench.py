@@ -179,11 +179,10 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
-    if cfg.B % world:
-        raise SystemExit(f"B={cfg.B} not divisible by {world} ranks")
-    B = cfg.B // world
+    from paper_2507_17245_b200.shard import batch_shard, max_over_ranks
+    b0, B = batch_shard(cfg.B, rank, world)
     G = cfg.group_size
-    q, k, v = make_qkv(cfg, device=dev, B=B, head_offset=rank * B)
+    q, k, v = make_qkv(cfg, device=dev, B=B, head_offset=b0)
     out = torch.empty_like(q)
     ws = torch.empty(da.distr_attn_workspace_size(tuple(q.shape), cfg.H_kv, block_l=cfg.block_l,
                                                   group_size=G), dtype=torch.uint8, device=dev)
@@ -209,6 +208,9 @@ def main():
             step(exact)
         launches_per_step = da.last_launch_count()
         evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+        for e3 in evs:  # torch creates the cudaEvent_t lazily: force creation before handing it over
+            for e in e3:
+                e.record(stream)
         barrier()
         t0 = torch.cuda.Event(enable_timing=True)
         t1 = torch.cuda.Event(enable_timing=True)
@@ -221,12 +223,7 @@ def main():
         total = t0.elapsed_time(t1)
         attn = [e[1].elapsed_time(e[2]) for e in evs]
         prep = [e[0].elapsed_time(e[1]) for e in evs]
-        if world > 1:
-            t = torch.tensor([total, float(np.mean(attn)), float(np.mean(prep))], device=dev)
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            total, a_ms, p_ms = t.tolist()
-        else:
-            a_ms, p_ms = float(np.mean(attn)), float(np.mean(prep))
+        total, a_ms, p_ms = max_over_ranks([total, np.mean(attn), np.mean(prep)], device=dev)
         return total / args.steps, a_ms, p_ms, launches_per_step, clk.summary()
 
     ms, attn_ms, prep_ms, lps, clocks = timed(False)
@@ -277,11 +274,7 @@ def main():
             da.distr_attn_fwd_host(qh, kh, vh, oh, block_l=cfg.block_l, group_size=G)
         e1.record(stream)
         barrier()
-        e_ms = e0.elapsed_time(e1) / n_e2e
-        if world > 1:
-            t = torch.tensor([e_ms], device=dev)
-            torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-            e_ms = t.item()
+        e_ms = max_over_ranks([e0.elapsed_time(e1) / n_e2e], device=dev)[0]
         nbytes = q.numel() * q.element_size()
         e2e = {"value": e_ms, "unit": "ms", "h2d_bytes_per_step": 3 * nbytes * world,
                "d2h_bytes_per_step": nbytes * world, "steps": n_e2e,

@@ -31,9 +31,15 @@ def _ptr(t):
 
 def make_params(q: torch.Tensor, k: torch.Tensor, *, block_l: int, group_size: int, seed: int = 0,
                 causal: bool = False, scale: float = 0.0, lse=None, bucket_ids=None, perm=None,
-                workspace=None) -> DaParams:
+                workspace=None, v=None, out=None) -> DaParams:
     if q.dim() != 4 or k.dim() != 4:
         raise ValueError("q must be [B,H,N,d] and k/v [B,H_kv,N,d]")
+    if k.shape[0] != q.shape[0] or k.shape[2:] != q.shape[2:] or k.dtype != q.dtype:
+        raise ValueError(f"k {tuple(k.shape)} does not match q {tuple(q.shape)}")
+    for t in (v, out):
+        if t is not None and (t.dtype != q.dtype or
+                              tuple(t.shape) != (tuple(k.shape) if t is v else tuple(q.shape))):
+            raise ValueError("v must match k and out must match q (shape and dtype)")
     if q.dtype not in _DT:
         raise ValueError(f"unsupported dtype {q.dtype}")
     B, H, N, d = q.shape
@@ -68,7 +74,8 @@ def distr_attn_fwd_ex(q, k, v, out=None, *, block_l=128, group_size=2, seed=0, c
     if out is None:
         out = torch.empty_like(q)
     p = make_params(q, k, block_l=block_l, group_size=group_size, seed=seed, causal=causal,
-                    scale=scale, lse=lse, bucket_ids=bucket_ids, perm=perm, workspace=workspace)
+                    scale=scale, lse=lse, bucket_ids=bucket_ids, perm=perm, workspace=workspace,
+                    v=v, out=out)
     check(_native.lib().distr_attn_fwd_ex(_ptr(q), _ptr(k), _ptr(v), _ptr(out), ctypes.byref(p),
                                           _stream(stream)))
     return out
@@ -81,7 +88,7 @@ def exact_attn_fwd_ex(q, k, v, out=None, *, block_l=128, causal=False, scale=0.0
     if out is None:
         out = torch.empty_like(q)
     p = make_params(q, k, block_l=block_l, group_size=1, causal=causal, scale=scale, lse=lse,
-                    workspace=workspace)
+                    workspace=workspace, v=v, out=out)
     check(_native.lib().exact_attn_fwd_ex(_ptr(q), _ptr(k), _ptr(v), _ptr(out), ctypes.byref(p),
                                           _stream(stream)))
     return out
@@ -89,6 +96,9 @@ def exact_attn_fwd_ex(q, k, v, out=None, *, block_l=128, causal=False, scale=0.0
 
 def distr_attn_fwd(q, k, v, out, B, H, N, d, block_l, group_size, seed):
     """North-star signature (legacy default stream, bf16, H_kv = H, non-causal)."""
+    for t in (q, k, v, out):
+        if tuple(t.shape) != (B, H, N, d) or t.dtype != torch.bfloat16 or not t.is_contiguous():
+            raise ValueError("distr_attn_fwd expects contiguous bf16 [B,H,N,d] q/k/v/out")
     check(_native.lib().distr_attn_fwd(_ptr(q), _ptr(k), _ptr(v), _ptr(out), B, H, N, d, block_l,
                                        group_size, seed))
     return out
@@ -104,7 +114,7 @@ def distr_attn_fwd_host(q, k, v, out=None, *, block_l=128, group_size=2, seed=0,
     if out is None:
         out = torch.empty_like(q)
     p = make_params(q, k, block_l=block_l, group_size=group_size, seed=seed, causal=causal,
-                    scale=scale, lse=lse)
+                    scale=scale, lse=lse, v=v, out=out)
     check(_native.lib().distr_attn_fwd_host(_ptr(q), _ptr(k), _ptr(v), _ptr(out), ctypes.byref(p),
                                             _stream(stream)))
     return out

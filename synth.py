@@ -60,34 +60,43 @@ def make_qkv(cfg: Config, *, dist: str = "normal", device="cpu", seed: int | Non
              head_offset: int = 0, B: int | None = None):
     """Q [B,H,N,d], K/V [B,H_kv,N,d] in cfg.dtype on `device`.
 
-    The generator is seeded from (seed, head_offset) so a rank can generate only its own shard
-    (multi-GPU: head_offset = first global batch index of the shard).
+    Every batch element b is drawn from its own generator seeded by (seed, head_offset + b), so
+    a rank that generates only its batch slice (multi-GPU: head_offset = first global batch
+    index of the shard) gets exactly the rows the full single-process tensor would hold.
     """
     seed = cfg.data_seed if seed is None else seed
     B = cfg.B if B is None else B
     dt = torch_dtype(cfg.dtype)
-    g = torch.Generator(device=device)
-    g.manual_seed(seed * 1_000_003 + head_offset)
-    shp_q = (B, cfg.H, cfg.N, cfg.d)
-    shp_kv = (B, cfg.H_kv, cfg.N, cfg.d)
+    qs, ks, vs = [], [], []
+    for bi in range(B):
+        g = torch.Generator(device=device)
+        g.manual_seed(seed * 1_000_003 + head_offset + bi)
+        q, k, v = _draw(cfg, dist, g, device)
+        qs.append(q.to(dt))
+        ks.append(k.to(dt))
+        vs.append(v.to(dt))
+    return torch.stack(qs).contiguous(), torch.stack(ks).contiguous(), torch.stack(vs).contiguous()
+
+
+def _draw(cfg: Config, dist: str, g: torch.Generator, device):
+    shp_q = (cfg.H, cfg.N, cfg.d)
+    shp_kv = (cfg.H_kv, cfg.N, cfg.d)
     if dist == "normal":
-        q = torch.randn(shp_q, generator=g, device=device, dtype=torch.float32)
-        k = torch.randn(shp_kv, generator=g, device=device, dtype=torch.float32)
-        v = torch.randn(shp_kv, generator=g, device=device, dtype=torch.float32)
-    elif dist == "uniform":
-        q = torch.rand(shp_q, generator=g, device=device, dtype=torch.float32)
-        k = torch.rand(shp_kv, generator=g, device=device, dtype=torch.float32)
-        v = torch.rand(shp_kv, generator=g, device=device, dtype=torch.float32)
-    elif dist == "clustered":
+        return (torch.randn(shp_q, generator=g, device=device),
+                torch.randn(shp_kv, generator=g, device=device),
+                torch.randn(shp_kv, generator=g, device=device))
+    if dist == "uniform":
+        return (torch.rand(shp_q, generator=g, device=device),
+                torch.rand(shp_kv, generator=g, device=device),
+                torch.rand(shp_kv, generator=g, device=device))
+    if dist == "clustered":
         nc = max(1, cfg.d // 4)
-        centres = torch.randn((B, cfg.H, cfg.N, nc), generator=g, device=device)
+        centres = torch.randn((cfg.H, cfg.N, nc), generator=g, device=device)
         assign = torch.randint(0, nc, (cfg.d,), generator=g, device=device)
         q = centres[..., assign] + 0.1 * torch.randn(shp_q, generator=g, device=device)
-        k = torch.randn(shp_kv, generator=g, device=device, dtype=torch.float32)
-        v = torch.randn(shp_kv, generator=g, device=device, dtype=torch.float32)
-    else:
-        raise ValueError(f"unknown dist {dist!r}")
-    return q.to(dt).contiguous(), k.to(dt).contiguous(), v.to(dt).contiguous()
+        return (q, torch.randn(shp_kv, generator=g, device=device),
+                torch.randn(shp_kv, generator=g, device=device))
+    raise ValueError(f"unknown dist {dist!r}")
 
 
 def sample_items(cfg: Config, n_heads: int = 4, per_head: int = 4, seed: int = 7):

@@ -179,7 +179,7 @@ def test_lse_and_host_entry_point():
 
 
 def test_north_star_entry_point_and_determinism():
-    cfg = cfg_small(N=1000, d=128, block_l=128, H=4)
+    cfg = cfg_small(N=1000, d=128, block_l=128, H=4, H_kv=4)  # north-star ABI: H_kv == H
     q, k, v = make_qkv(cfg, device=DEV)
     out = torch.empty_like(q)
     torch.cuda.synchronize()

@@ -1,0 +1,16 @@
+#!/bin/bash
+# One GPU session: tests, smoke, bench, ncu launch list + full capture. Logs under gpurun_out/.
+set -x
+O=gpurun_out
+mkdir -p $O
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,driver_version --format=csv > $O/gpu.txt
+python -c "import __graft_entry__ as g; g.build()" > $O/build.log 2>&1
+if [[ "$1" != "nobench-tests" ]]; then
+timeout -s KILL 1200 python -m pytest tests -m gpu -x -q -p no:cacheprovider > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log
+fi
+timeout -s KILL 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/smoke.log
+timeout -s KILL 900 python bench.py > $O/bench.log 2>&1; echo "bench rc=$?" >> $O/bench.log
+timeout -s KILL 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 60 --csv --log-file $O/launches.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu --no-parity > $O/ncu_launches.log 2>&1
+timeout -s KILL 900 ncu --set full --clock-control none --import-source on -k regex:attn_kernel -s 3 -c 1 -o $O/prof_attn -f python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --no-parity > $O/ncu_full_attn.log 2>&1
+timeout -s KILL 600 ncu --set full --clock-control none --import-source on -k regex:prep_kernel -s 3 -c 1 -o $O/prof_prep -f python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --no-parity > $O/ncu_full_prep.log 2>&1
+ls -la $O
