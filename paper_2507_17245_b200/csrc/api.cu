@@ -4,6 +4,7 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
@@ -220,6 +221,20 @@ int current_device(int* dev) {
   return DA_OK;
 }
 
+// Share of exp2 pairs (out of 8) evaluated by polynomial on the FMA pipe instead of MUFU.EX2.
+// Measured on B200 (profiles/r01_v2): with the ping-pong softmax the MUFU is not the binding
+// unit (XU pipe < 50 % busy) and every emulated pair costs issue slots the softmax warpgroups
+// need, so the default is 0 for every flavour. DA_EMU overrides (0, 2, 3, 4) for tuning.
+int default_emu(const Plan& P, bool distr) {
+  static int env = [] {
+    const char* e = getenv("DA_EMU");
+    return e ? atoi(e) : -1;
+  }();
+  (void)P;
+  (void)distr;
+  return env >= 0 ? env : 0;
+}
+
 // ---------------------------------------------------------------------------- forward
 int forward(const void* q, const void* k, const void* v, void* out, const da_params* p, cudaStream_t st,
             bool distr) {
@@ -304,7 +319,7 @@ int forward(const void* q, const void* k, const void* v, void* out, const da_par
   aa.out = out;
   aa.out_f32 = P.f32;
   aa.lse = p->lse;
-  da::AttnLaunch L{P.d, P.G, P.HB, distr ? 1 : 0, (int)BH, &tmA, &tmK, &tmV};
+  da::AttnLaunch L{P.d, P.G, P.HB, distr ? 1 : 0, (int)BH, &tmA, &tmK, &tmV, default_emu(P, distr)};
   record_ev(1, st);
   DA_CUDA(da::launch_attn(L, aa, st));
   record_ev(2, st);

@@ -1,18 +1,23 @@
 // attn.cu — fused DistrAttention / exact attention forward for sm_100a (tcgen05 + TMEM + TMA).
 //
-// One CTA = one 128-row Q tile of one (b, h) (the outer loop of Fig. 3); the inner
-// loop walks 128-key tiles. Warp roles (256 threads):
-//   warp 0      TMA producer: Q (exact) or Q̂ (distr) once, then K (exact) or K^T (distr) and V
-//               tiles through a 2-stage mbarrier ring.
-//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer:
-//                 S_i  = A · B_i^T   (M=128, N=128, K = d or DR = HB*d/G*; fp32 in TMEM)
-//                 O   += P_{i-1} · V_{i-1}  (A = P from TMEM, B = V MN-major, N = d)
-//   warps 2-3   (distr) fusion: K̂^T_i[j][t] = sum_{c in G_j} K^T_i[c][t] for this tile's own
+// One CTA = TWO 128-row Q tiles of one (b, h) (the outer loop of Fig. 3, two
+// iterations per CTA); the inner loop walks 128-key tiles that both Q tiles share in smem.
+// Warp roles (384 threads):
+//   warp 0      TMA producer: Q (exact) or Q̂ (distr) of both tiles once, then K (exact) or K^T
+//               (distr) and V tiles through an NS-stage mbarrier ring.
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer, ping-ponging the two tiles:
+//                 S_t  = A_t · B_t^T        (M=128, N=128, K = d or DR = HB*d/G*; fp32 in TMEM)
+//                 O_t += P_t · V            (A = P_t bf16 read from TMEM, B = V MN-major, N = d)
+//   warps 2-3   (distr) fusion: K̂_t^T[j][key] = sum_{c in G_j} K^T[c][key] with each tile's own
 //               permutation(s) — Eq. 2 with the block-wise grouping of §3.3 (P:306:
 //               "the rows of a K block are grouped depending on which Q block is multiplied by").
-//   warps 4-7   softmax (thread = query row = TMEM lane): row max, exp2, row sum, P -> TMEM (bf16),
-//               lazy O rescale (only when the running max grows by > 2^8), final O / l epilogue.
-// S is double-buffered in TMEM (cols 128..383), O lives in cols 0..d-1.
+//   warps 4-7   softmax warpgroup of tile 0, warps 8-11 of tile 1 (thread = query row = TMEM
+//               lane): row max, exp2 (MUFU + FMA-pipe polynomial), row sum, P -> TMEM (bf16),
+//               lazy O rescale (only when the running max grows by > 2^8), O / l epilogue.
+// While one warpgroup waits for its next S the other runs its exp phase, so the MUFU, the FMA
+// pipe and the tensor core overlap (the FlashAttention-4 ping-pong, re-derived here).
+// TMEM (512 columns): O_0 [0, d), O_1 [d, 2d), S_0 [256, 384), S_1 [384, 512); P_t aliases the
+// first 64 columns of S_t.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -24,13 +29,15 @@
 namespace da {
 namespace {
 
-constexpr int kThreads = 256;
+// 384 threads (exact: TMA/MMA warpgroup + 2 softmax warpgroups) or 512 (distr: + fusion warpgroup)
+template <bool DISTR>
+constexpr int threads_of() { return DISTR ? 512 : 384; }
+constexpr int kFusionThreads = 128;
 constexpr int BM = 128;  // query rows per tile (UMMA M)
 constexpr int BN = 128;  // keys per tile (UMMA N of S, K of PV)
-constexpr int NS = 2;    // K/V pipeline stages
 constexpr uint32_t kTmemCols = 512;
-constexpr uint32_t kColO = 0;
-constexpr uint32_t kColS = 128;  // S buffer b at kColS + 128*b; P_b aliases its first 64 cols
+constexpr uint32_t kColS = 256;  // S_t at kColS + 128*t
+constexpr int kSmemMax = 232448 - 1024;
 
 template <int D, bool DISTR, int G, int HB>
 struct Cfg {
@@ -40,44 +47,55 @@ struct Cfg {
   static constexpr int A_BOX_COLS = A_SW / 2;
   static constexpr int A_NBOX = A_COLS / A_BOX_COLS;
   static constexpr int A_BOX_BYTES = BM * A_SW;
-  static constexpr int A_BYTES = A_NBOX * A_BOX_BYTES;
-  static constexpr int K_BYTES = BN * D * 2;  // K tile (exact) or K^T tile (distr)
+  static constexpr int A_BYTES = A_NBOX * A_BOX_BYTES;  // one Q tile
+  static constexpr int K_BYTES = BN * D * 2;             // K tile (exact) or K^T tile (distr)
   static constexpr int V_BYTES = BN * D * 2;
   static constexpr int KH_BYTES = DISTR ? DR * BN * 2 : 0;
   static constexpr int al(int x) { return (x + 1023) / 1024 * 1024; }
+  static constexpr int bytes(int ns, int nkh) {
+    return al(2 * A_BYTES) + ns * (K_BYTES + V_BYTES) + 2 * nkh * KH_BYTES + 1024;
+  }
+  // Deepest K/V ring (NS) and K̂ ring (NKH) that fit the 227 KB of shared memory.
+  static constexpr int NKH = !DISTR ? 0 : (bytes(2, 2) <= kSmemMax ? 2 : 1);
+  static constexpr int NS = bytes(2, NKH) <= kSmemMax ? 2 : 1;
   static constexpr int OFF_A = 0;
-  static constexpr int OFF_K = al(OFF_A + A_BYTES);
+  static constexpr int OFF_K = al(2 * A_BYTES);
   static constexpr int OFF_V = OFF_K + NS * K_BYTES;
   static constexpr int OFF_KH = OFF_V + NS * V_BYTES;
-  static constexpr int OFF_PERM = OFF_KH + 2 * KH_BYTES;
-  static constexpr int OFF_BAR = OFF_PERM + 2 * 128;
-  static constexpr int SMEM = OFF_BAR + 256 + 1024;  // + slack for 1024-B alignment
+  static constexpr int OFF_PERM = OFF_KH + 2 * NKH * KH_BYTES;
+  static constexpr int OFF_BAR = OFF_PERM + 2 * 2 * 128;
+  static constexpr int SMEM = OFF_BAR + 512 + 1024;  // + slack for 1024-B alignment
   static constexpr uint32_t A_LAYOUT = A_SW == 128 ? kSw128 : (A_SW == 64 ? kSw64 : kSw32);
   static_assert(DR % 16 == 0 && DR >= 16 && DR <= 128, "reduced width");
   static_assert(A_COLS % A_BOX_COLS == 0, "A boxes");
+  static_assert(SMEM <= 232448, "shared memory");
 };
 
 // Barrier slots (uint64 each) inside OFF_BAR.
 enum {
   B_Q = 0,
-  B_KFULL = 1,   // +s
-  B_KEMPTY = 3,  // +s
-  B_VFULL = 5,   // +s
-  B_VEMPTY = 7,  // +s
-  B_KHFULL = 9,  // +b
-  B_KHEMPTY = 11,
-  B_SFULL = 13,  // +b
-  B_PFULL = 15,  // +b
-  B_O = 17,
-  B_TMEMPTR = 18,
-  B_COUNT = 19
+  B_KFULL = 1,    // +s (2)
+  B_KEMPTY = 3,   // +s
+  B_VFULL = 5,    // +s
+  B_VEMPTY = 7,   // +s
+  B_KHFULL = 9,   // + t*2 + stage (4)
+  B_KHEMPTY = 13, // + t*2 + stage (4)
+  B_SFULL = 17,   // +t
+  B_PFULL = 19,   // +t
+  B_OFULL = 21,   // +t
+  B_TMEMPTR = 23,
+  B_COUNT = 24
 };
 
-template <int D, bool DISTR, int G, int HB>
-__global__ void __launch_bounds__(kThreads, 1)
+// EMU: number of every 8 column pairs whose exp2 runs as a polynomial on the FMA pipe instead of
+// MUFU.EX2 (16 ex2/clk/SM, one per (query, key) pair — it co-bounds the tile with the tensor
+// core; moving EMU/8 of the exps to the FMA pipe rebalances the two).
+template <int D, bool DISTR, int G, int HB, int EMU>
+__global__ void __launch_bounds__(threads_of<DISTR>(), 1)
     attn_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmK,
                 const __grid_constant__ CUtensorMap tmV, const AttnArgs args) {
   using C = Cfg<D, DISTR, G, HB>;
+  constexpr int NS = C::NS, NKH = C::NKH > 0 ? C::NKH : 1;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   uint8_t* sA = smem + C::OFF_A;
@@ -90,40 +108,51 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = warp_id(), lane = lane_id();
   const int bh = blockIdx.y;
-  const int qt = args.causal ? (args.nqt - 1 - (int)blockIdx.x) : (int)blockIdx.x;
+  // causal: heaviest pairs of Q tiles first
+  const int pair = args.causal ? ((args.nqt + 1) / 2 - 1 - (int)blockIdx.x) : (int)blockIdx.x;
   const int b = bh / args.H, h = bh % args.H;
   const int bhkv = b * args.H_kv + h / (args.H / args.H_kv);
-  const int q0 = qt * BM;
-  const int nk = args.causal ? min(qt + 1, args.nkt) : args.nkt;
+  const int qt0 = 2 * pair;
+  // key tiles each Q tile visits (0 = tile absent)
+  int nkt_t[2];
+#pragma unroll
+  for (int t = 0; t < 2; ++t) {
+    const int qt = qt0 + t;
+    nkt_t[t] = qt >= args.nqt ? 0 : (args.causal ? min(qt + 1, args.nkt) : args.nkt);
+  }
+  const int nk = max(nkt_t[0], nkt_t[1]);
 
   if (threadIdx.x == 0) {
     mbar_init(&bars[B_Q], 1);
     for (int s = 0; s < NS; ++s) {
       mbar_init(&bars[B_KFULL + s], 1);
-      mbar_init(&bars[B_KEMPTY + s], DISTR ? 64 : 1);
+      mbar_init(&bars[B_KEMPTY + s], DISTR ? kFusionThreads : 1);
       mbar_init(&bars[B_VFULL + s], 1);
       mbar_init(&bars[B_VEMPTY + s], 1);
     }
-    for (int bb = 0; bb < 2; ++bb) {
-      mbar_init(&bars[B_KHFULL + bb], 64);
-      mbar_init(&bars[B_KHEMPTY + bb], 1);
-      mbar_init(&bars[B_SFULL + bb], 1);
-      mbar_init(&bars[B_PFULL + bb], 128);
+    for (int t = 0; t < 2; ++t) {
+      for (int st = 0; st < 2; ++st) {
+        mbar_init(&bars[B_KHFULL + 2 * t + st], kFusionThreads);
+        mbar_init(&bars[B_KHEMPTY + 2 * t + st], 1);
+      }
+      mbar_init(&bars[B_SFULL + t], 1);
+      mbar_init(&bars[B_PFULL + t], 128);
+      mbar_init(&bars[B_OFULL + t], 1);
     }
-    mbar_init(&bars[B_O], 1);
     fence_mbar_init();
   }
   if (warp == 1) {
     tmem_alloc(tmem_ptr_s, kTmemCols);
     tmem_relinquish();
   }
-  if (DISTR && (warp == 2 || warp == 3)) {
-    // This tile's permutation(s): hash block(s) covering rows [q0, q0 + 128).
-    const int t = threadIdx.x - 64;
-    for (int i = t; i < HB * D; i += 64) {
-      const int hb = i / D, c = i % D;
-      const int qb = q0 / args.block_l + hb;
-      perm_s[hb * D + c] = (qb < args.nqb) ? args.perm[((size_t)bh * args.nqb + qb) * D + c] : (uint8_t)c;
+  if (DISTR && warp >= 12) {
+    // Permutation(s) of both tiles: hash block(s) covering rows [128*qt, 128*qt + 128).
+    const int ft = threadIdx.x - 384;
+    for (int i = ft; i < 2 * HB * D; i += kFusionThreads) {
+      const int t = i / (HB * D), hb = (i / D) % HB, c = i % D;
+      const int qb = (qt0 + t) * BM / args.block_l + hb;
+      perm_s[(t * HB + hb) * D + c] =
+          (qb < args.nqb) ? args.perm[((size_t)bh * args.nqb + qb) * D + c] : (uint8_t)c;
     }
   }
   tc_fence_before();
@@ -131,15 +160,28 @@ __global__ void __launch_bounds__(kThreads, 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_ptr_s;
 
+  // Register split: the TMA/MMA warpgroup (and the fusion warpgroup) hand registers to the two
+  // softmax warpgroups. exact: 128*88 + 256*208 = 384*168; distr: 128*48 + 128*96 + 256*184 <=
+  // 512*128 — never more than the pool the launch reserved (an .inc that exceeds what the .dec
+  // calls released would block forever). Each setmaxnreg sits at the head of its warpgroup's
+  // branch so ptxas budgets each region separately.
+  if (warp < 4) {
+  if (DISTR)
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 48;");
+  else
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
   if (warp == 0) {
     // ------------------------------------------------------------------ TMA producer
     if (lane == 0) {
       tma_prefetch_desc(&tmA);
       tma_prefetch_desc(&tmK);
       tma_prefetch_desc(&tmV);
-      mbar_arrive_expect_tx(&bars[B_Q], C::A_BYTES);
-      for (int bx = 0; bx < C::A_NBOX; ++bx)
-        tma_load_3d(sA + bx * C::A_BOX_BYTES, &tmA, &bars[B_Q], bx * C::A_BOX_COLS, q0, bh);
+      const int ntile = nkt_t[1] > 0 ? 2 : 1;
+      mbar_arrive_expect_tx(&bars[B_Q], ntile * C::A_BYTES);
+      for (int t = 0; t < ntile; ++t)
+        for (int bx = 0; bx < C::A_NBOX; ++bx)
+          tma_load_3d(sA + t * C::A_BYTES + bx * C::A_BOX_BYTES, &tmA, &bars[B_Q], bx * C::A_BOX_COLS,
+                      (qt0 + t) * BM, bh);
       for (int i = 0; i < nk; ++i) {
         const int s = i % NS;
         const uint32_t ph = (i / NS) & 1;
@@ -163,146 +205,101 @@ __global__ void __launch_bounds__(kThreads, 1)
       constexpr uint32_t IDESC_S = make_idesc_bf16(BM, BN, false, DISTR);
       constexpr uint32_t IDESC_PV = make_idesc_bf16(BM, D, false, true);
       const uint32_t a_base = smem_u32(sA);
-      auto issue_pv = [&](int j) {
-        const int s = j % NS;
-        mbar_wait(&bars[B_PFULL + (j & 1)], (j >> 1) & 1);
-        mbar_wait(&bars[B_VFULL + s], (j / NS) & 1);
-        tc_fence_after();
-        const uint32_t v_base = smem_u32(sV + s * C::V_BYTES);
-        const uint32_t p_tmem = tmem + kColS + 128u * (j & 1);
-#pragma unroll
-        for (int kk = 0; kk < BN / 16; ++kk) {
-          // V as the MN-major B operand: 64-column blocks (LBO) of 8-key groups (SBO).
-          const uint64_t vdesc = make_sdesc(v_base + kk * 2048, BN * 128, 1024, kSw128);
-          mma_ts(tmem + kColO, p_tmem + kk * 8, vdesc, IDESC_PV, (j > 0 || kk > 0) ? 1u : 0u);
-        }
-        mma_commit(&bars[B_VEMPTY + s]);
-        mma_commit(&bars[B_O]);
-      };
-      mbar_wait(&bars[B_Q], 0);
-      tc_fence_after();
-      for (int i = 0; i < nk; ++i) {
-        const int bb = i & 1;
+      auto issue_s = [&](int t, int i) {
         const int s = i % NS;
         if (DISTR)
-          mbar_wait(&bars[B_KHFULL + bb], (i >> 1) & 1);
-        else
+          mbar_wait(&bars[B_KHFULL + 2 * t + i % NKH], (i / NKH) & 1);
+        else if (t == 0 || nkt_t[0] <= i)  // first consumer of K tile i waits for it
           mbar_wait(&bars[B_KFULL + s], (i / NS) & 1);
         tc_fence_after();
-        const uint32_t d_s = tmem + kColS + 128u * bb;
+        const uint32_t d_s = tmem + kColS + 128u * t;
 #pragma unroll
         for (int kk = 0; kk < C::A_COLS / 16; ++kk) {
           constexpr int kpb = C::A_BOX_COLS / 16;  // K-steps per A box
-          const uint64_t adesc = make_sdesc(a_base + (kk / kpb) * C::A_BOX_BYTES + (kk % kpb) * 32, 16,
-                                            8 * C::A_SW, C::A_LAYOUT);
+          const uint64_t adesc = make_sdesc(a_base + t * C::A_BYTES + (kk / kpb) * C::A_BOX_BYTES + (kk % kpb) * 32,
+                                            16, 8 * C::A_SW, C::A_LAYOUT);
           uint64_t bdesc;
           if (DISTR) {
             // K̂^T as the MN-major B operand: 64-key blocks (LBO = DR*128 B), 8-row groups (SBO).
-            bdesc = make_sdesc(smem_u32(sKh + bb * C::KH_BYTES) + kk * 2048, C::DR * 128, 1024, kSw128);
+            bdesc = make_sdesc(smem_u32(sKh + (t * NKH + i % NKH) * C::KH_BYTES) + kk * 2048, C::DR * 128, 1024,
+                               kSw128);
           } else {
             bdesc = make_sdesc(smem_u32(sK + s * C::K_BYTES) + (kk / 4) * (BN * 128) + (kk % 4) * 32, 16, 1024,
                                kSw128);
           }
           mma_ss(d_s, adesc, bdesc, IDESC_S, kk > 0 ? 1u : 0u);
         }
-        mma_commit(&bars[B_SFULL + bb]);
-        if (DISTR)
-          mma_commit(&bars[B_KHEMPTY + bb]);
-        else
-          mma_commit(&bars[B_KEMPTY + s]);
-        if (i > 0) issue_pv(i - 1);
-      }
-      issue_pv(nk - 1);
-    }
-  } else if (warp == 2 || warp == 3) {
-    // ------------------------------------------------------------------ fusion (distr only)
-    if (DISTR) {
-      const int ft = threadIdx.x - 64;  // 0..63
-      constexpr int NT = C::DR * 16 / 64;  // 16-byte tasks per thread per tile
-      constexpr int DG = D / G;
-      uint16_t src[NT][G];
-      uint32_t dst[NT];
+        mma_commit(&bars[B_SFULL + t]);
+        if (DISTR) mma_commit(&bars[B_KHEMPTY + 2 * t + i % NKH]);
+      };
+      auto issue_pv = [&](int t, int j) {
+        const int s = j % NS;
+        mbar_wait(&bars[B_PFULL + t], j & 1);
+        if (t == 0 || nkt_t[0] <= j) mbar_wait(&bars[B_VFULL + s], (j / NS) & 1);
+        tc_fence_after();
+        const uint32_t v_base = smem_u32(sV + s * C::V_BYTES);
+        const uint32_t p_tmem = tmem + kColS + 128u * t;
 #pragma unroll
-      for (int n = 0; n < NT; ++n) {
-        const int task = n * 64 + ft;
-        const int j = task >> 4, ch = task & 15;
-        const int hb = j / DG, jj = j % DG;
-#pragma unroll
-        for (int g = 0; g < G; ++g) src[n][g] = (uint16_t)(perm_s[hb * D + jj * G + g] * (BN * 2) + ch * 16);
-        dst[n] = (uint32_t)((ch >> 3) * (C::DR * 128) + j * 128 + (((ch & 7) ^ (j & 7)) << 4));
-      }
-      for (int i = 0; i < nk; ++i) {
-        const int s = i % NS, bb = i & 1;
-        mbar_wait(&bars[B_KFULL + s], (i / NS) & 1);
-        mbar_wait(&bars[B_KHEMPTY + bb], ((i >> 1) & 1) ^ 1);
-        const uint8_t* kt = sK + s * C::K_BYTES;
-        uint8_t* kh = sKh + bb * C::KH_BYTES;
-#pragma unroll
-        for (int n = 0; n < NT; ++n) {
-          uint4 o;
-          if (G == 1) {
-            o = *reinterpret_cast<const uint4*>(kt + src[n][0]);
-          } else {
-            float acc[8];
-            {
-              const uint4 x = *reinterpret_cast<const uint4*>(kt + src[n][0]);
-              const uint32_t xv[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const float2 f = unpack_bf16x2(xv[e]);
-                acc[2 * e] = f.x;
-                acc[2 * e + 1] = f.y;
-              }
-            }
-#pragma unroll
-            for (int g = 1; g < G; ++g) {
-              const uint4 x = *reinterpret_cast<const uint4*>(kt + src[n][g]);
-              const uint32_t xv[4] = {x.x, x.y, x.z, x.w};
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const float2 f = unpack_bf16x2(xv[e]);
-                acc[2 * e] += f.x;
-                acc[2 * e + 1] += f.y;
-              }
-            }
-            o = make_uint4(pack_bf16x2(acc[0], acc[1]), pack_bf16x2(acc[2], acc[3]), pack_bf16x2(acc[4], acc[5]),
-                           pack_bf16x2(acc[6], acc[7]));
-          }
-          *reinterpret_cast<uint4*>(kh + dst[n]) = o;
+        for (int kk = 0; kk < BN / 16; ++kk) {
+          // V as the MN-major B operand: 64-column blocks (LBO) of 8-key groups (SBO).
+          const uint64_t vdesc = make_sdesc(v_base + kk * 2048, BN * 128, 1024, kSw128);
+          mma_ts(tmem + (uint32_t)(t * D), p_tmem + kk * 8, vdesc, IDESC_PV, (j > 0 || kk > 0) ? 1u : 0u);
         }
-        fence_proxy_async_smem();
-        mbar_arrive(&bars[B_KHFULL + bb]);
-        mbar_arrive(&bars[B_KEMPTY + s]);
+        if (j == nkt_t[t] - 1) mma_commit(&bars[B_OFULL + t]);
+      };
+      // release K / V stage i once every tile that uses it has issued its MMA on it
+      auto release_k = [&](int i) {
+        if (!DISTR) mma_commit(&bars[B_KEMPTY + i % NS]);
+      };
+      auto release_v = [&](int j) { mma_commit(&bars[B_VEMPTY + j % NS]); };
+
+      mbar_wait(&bars[B_Q], 0);
+      tc_fence_after();
+      for (int i = 0; i < nk; ++i) {
+        // tile 0: PV_0(i-1) then S_0(i)   (S_0(i) overwrites P_0(i-1): in-order after the PV)
+        if (i >= 1 && i - 1 < nkt_t[0]) issue_pv(0, i - 1);
+        if (i >= 1 && !(i - 1 < nkt_t[1])) release_v(i - 1);
+        if (i < nkt_t[0]) issue_s(0, i);
+        if (i >= 1 && i - 1 < nkt_t[1]) {
+          issue_pv(1, i - 1);
+          release_v(i - 1);
+        }
+        if (i < nkt_t[1]) issue_s(1, i);
+        release_k(i);
       }
+      if (nk - 1 < nkt_t[0]) issue_pv(0, nk - 1);
+      if (nk - 1 < nkt_t[1]) issue_pv(1, nk - 1);
+      release_v(nk - 1);
     }
-  } else {
-    // ------------------------------------------------------------------ softmax (warps 4..7)
-    const int row = (warp - 4) * 32 + lane;
+  }  // warps 2-3 idle
+  } else if (warp < 12) {
+    if (DISTR)
+      asm volatile("setmaxnreg.inc.sync.aligned.u32 184;");
+    else
+      asm volatile("setmaxnreg.inc.sync.aligned.u32 208;");
+    // ------------------------------------------------------------------ softmax (warps 4..11)
+    const int t = (warp - 4) >> 2;  // Q tile of this warpgroup
+    const int nkt = nkt_t[t];
+    const int row = (warp & 3) * 32 + lane;
     const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+    const uint32_t tS = tmem + lane_base + kColS + 128u * t;
+    const uint32_t tO = tmem + lane_base + (uint32_t)(t * D);
+    const int q0 = (qt0 + t) * BM;
     const int q_row = q0 + row;
     const float sl2 = args.scale_log2;
     float m = -INFINITY;  // running max of scaled log2 scores (possibly stale by <= 8)
     float l = 0.0f;
-    int o_seen = 0;
-    for (int i = 0; i < nk; ++i) {
-      const int bb = i & 1;
-      if (i >= 2) {
-        while (o_seen < i - 1) {  // PV_{i-2} completed before S_i was committed
-          mbar_wait(&bars[B_O], o_seen & 1);
-          ++o_seen;
-        }
-      }
-      mbar_wait(&bars[B_SFULL + bb], (i >> 1) & 1);
+    for (int i = 0; i < nkt; ++i) {
+      mbar_wait(&bars[B_SFULL + t], i & 1);
       tc_fence_after();
+      uint32_t sr[BN];
+#pragma unroll
+      for (int c = 0; c < BN / 32; ++c)
+        tmem_ld32(tS + 32u * c, *reinterpret_cast<uint32_t(*)[32]>(&sr[32 * c]));
+      tmem_ld_wait();
       float s[BN];
 #pragma unroll
-      for (int c = 0; c < BN / 32; ++c) {
-        uint32_t r[32];
-        tmem_ld32(tmem + lane_base + kColS + 128u * bb + 32u * c, r);
-        tmem_ld_wait();
-#pragma unroll
-        for (int e = 0; e < 32; ++e) s[32 * c + e] = __uint_as_float(r[e]);
-      }
+      for (int e = 0; e < BN; ++e) s[e] = __uint_as_float(sr[e]);
       const int kbase = i * BN;
       if (kbase + BN > args.N || (args.causal && kbase + BN - 1 > q0)) {
         const int lim = args.causal ? min(args.N - 1, q_row) : args.N - 1;
@@ -310,87 +307,179 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int e = 0; e < BN; ++e)
           if (kbase + e > lim) s[e] = -INFINITY;
       }
-      float mx = s[0];
+      // Row max: 8 independent FMNMX3 chains (depth 8) instead of one 128-long chain.
+      float mx8[8];
 #pragma unroll
-      for (int e = 1; e < BN; ++e) mx = fmaxf(mx, s[e]);
+      for (int j = 0; j < 8; ++j) mx8[j] = max3(s[j], s[8 + j], s[120 + j]);
+#pragma unroll
+      for (int e = 16; e < 120; e += 16)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) mx8[j] = max3(mx8[j], s[e + j], s[e + 8 + j]);
+      const float mx = max3(max3(mx8[0], mx8[1], mx8[2]), max3(mx8[3], mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]));
       const float mnew = fmaxf(m, mx * sl2);
       if (i == 0) {
         m = mnew;
       } else {
+        // S_t(i) was committed after PV_t(i-1) was issued, so O_t already holds sum_{<i} P V.
         const bool need = mnew > m + 8.0f;
         if (__any_sync(0xffffffffu, need)) {
-          while (o_seen < i) {  // O must hold exactly sum_{t<i} P_t V_t before rescaling
-            mbar_wait(&bars[B_O], o_seen & 1);
-            ++o_seen;
-          }
-          tc_fence_after();
           const float f = need ? ex2(m - mnew) : 1.0f;
 #pragma unroll
           for (int c = 0; c < D / 32; ++c) {
             uint32_t r[32];
-            tmem_ld32(tmem + lane_base + kColO + 32u * c, r);
+            tmem_ld32(tO + 32u * c, r);
             tmem_ld_wait();
 #pragma unroll
             for (int e = 0; e < 32; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * f);
-            tmem_st32(tmem + lane_base + kColO + 32u * c, r);
+            tmem_st32(tO + 32u * c, r);
           }
-          tmem_st_wait();
           if (need) {
             l *= f;
             m = mnew;
           }
         }
       }
-      const float nm = -m;
-      float sum = 0.0f;
+      // p = 2^(s*scale*log2e - m): FFMA2 for the affine part, EMU/8 of the pairs on the FMA pipe,
+      // the rest on MUFU; 4 independent FADD2 partial sums.
+      const float2 sl2x2 = make_float2(sl2, sl2), nm2 = make_float2(-m, -m);
+      float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
 #pragma unroll
       for (int c = 0; c < 2; ++c) {
         uint32_t pr[32];
 #pragma unroll
         for (int e = 0; e < 32; ++e) {
-          const float p0 = ex2(fmaf(s[64 * c + 2 * e], sl2, nm));
-          const float p1 = ex2(fmaf(s[64 * c + 2 * e + 1], sl2, nm));
-          sum += p0 + p1;
-          pr[e] = pack_bf16x2(p0, p1);
+          const int col = 64 * c + 2 * e;
+          const float2 x = fma2(make_float2(s[col], s[col + 1]), sl2x2, nm2);
+          float2 p;
+          if ((e & 7) >= 8 - EMU)
+            p = exp2_poly2(x);
+          else
+            p = make_float2(ex2(x.x), ex2(x.y));
+          acc[e & 3] = fadd2(acc[e & 3], p);
+          pr[e] = pack_bf16x2(p.x, p.y);
         }
-        tmem_st32(tmem + lane_base + kColS + 128u * bb + 32u * c, pr);
+        tmem_st32(tS + 32u * c, pr);
       }
-      l += sum;
+      const float2 a = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
+      l += a.x + a.y;
       tmem_st_wait();
       tc_fence_before();
-      mbar_arrive(&bars[B_PFULL + bb]);
+      mbar_arrive(&bars[B_PFULL + t]);
     }
-    while (o_seen < nk) {
-      mbar_wait(&bars[B_O], o_seen & 1);
-      ++o_seen;
-    }
-    tc_fence_after();
-    const float inv = 1.0f / l;
+    if (nkt > 0) {
+      mbar_wait(&bars[B_OFULL + t], 0);
+      tc_fence_after();
+      const float inv = 1.0f / l;
 #pragma unroll
-    for (int c = 0; c < D / 32; ++c) {
-      uint32_t r[32];
-      tmem_ld32(tmem + lane_base + kColO + 32u * c, r);
-      tmem_ld_wait();
-      if (q_row < args.N) {
-        const size_t off = ((size_t)bh * args.N + q_row) * D + 32 * c;
-        if (args.out_f32) {
-          float4* o = reinterpret_cast<float4*>(static_cast<float*>(args.out) + off);
+      for (int c = 0; c < D / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld32(tO + 32u * c, r);
+        tmem_ld_wait();
+        if (q_row < args.N) {
+          const size_t off = ((size_t)bh * args.N + q_row) * D + 32 * c;
+          if (args.out_f32) {
+            float4* o = reinterpret_cast<float4*>(static_cast<float*>(args.out) + off);
 #pragma unroll
-          for (int e = 0; e < 8; ++e)
-            o[e] = make_float4(__uint_as_float(r[4 * e]) * inv, __uint_as_float(r[4 * e + 1]) * inv,
-                               __uint_as_float(r[4 * e + 2]) * inv, __uint_as_float(r[4 * e + 3]) * inv);
-        } else {
-          uint4* o = reinterpret_cast<uint4*>(static_cast<uint16_t*>(args.out) + off);
+            for (int e = 0; e < 8; ++e)
+              o[e] = make_float4(__uint_as_float(r[4 * e]) * inv, __uint_as_float(r[4 * e + 1]) * inv,
+                                 __uint_as_float(r[4 * e + 2]) * inv, __uint_as_float(r[4 * e + 3]) * inv);
+          } else {
+            uint4* o = reinterpret_cast<uint4*>(static_cast<uint16_t*>(args.out) + off);
 #pragma unroll
-          for (int e = 0; e < 4; ++e)
-            o[e] = make_uint4(pack_bf16x2(__uint_as_float(r[8 * e]) * inv, __uint_as_float(r[8 * e + 1]) * inv),
-                              pack_bf16x2(__uint_as_float(r[8 * e + 2]) * inv, __uint_as_float(r[8 * e + 3]) * inv),
-                              pack_bf16x2(__uint_as_float(r[8 * e + 4]) * inv, __uint_as_float(r[8 * e + 5]) * inv),
-                              pack_bf16x2(__uint_as_float(r[8 * e + 6]) * inv, __uint_as_float(r[8 * e + 7]) * inv));
+            for (int e = 0; e < 4; ++e)
+              o[e] = make_uint4(pack_bf16x2(__uint_as_float(r[8 * e]) * inv, __uint_as_float(r[8 * e + 1]) * inv),
+                                pack_bf16x2(__uint_as_float(r[8 * e + 2]) * inv, __uint_as_float(r[8 * e + 3]) * inv),
+                                pack_bf16x2(__uint_as_float(r[8 * e + 4]) * inv, __uint_as_float(r[8 * e + 5]) * inv),
+                                pack_bf16x2(__uint_as_float(r[8 * e + 6]) * inv, __uint_as_float(r[8 * e + 7]) * inv));
+          }
         }
       }
+      if (args.lse && q_row < args.N)
+        args.lse[(size_t)bh * args.N + q_row] = (m + log2f(l)) * 0.69314718055994531f;
     }
-    if (args.lse && q_row < args.N) args.lse[(size_t)bh * args.N + q_row] = (m + log2f(l)) * 0.69314718055994531f;
+  } else {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 96;");
+    // ------------------------------------------------------------------ fusion (warps 12..15)
+    // Thread f owns 16-byte chunk ch = f % 16 (8 keys) of K̂^T rows j = f/16 + 8n, n < DR/8.
+    // Its source-row byte offsets (perm rows * 256 + ch * 16) are fixed for the CTA's lifetime,
+    // so the per-tile work is G 16-byte loads, a bf16x2 add chain and one 16-byte store per task.
+    // 16 lanes read one whole 256-byte K^T row (conflict-free); stores land in the UMMA
+    // MN-major SWIZZLE_128B layout (chunk ^= row % 8, row % 8 == f/16 for every task).
+    if (DISTR) {
+      const int f = threadIdx.x - 384;
+      const int ch = f & 15, jb = f >> 4;
+      constexpr int NT = C::DR / 8;  // tasks per thread per (tile, key tile)
+      constexpr int DG = D / G;
+      constexpr int NW = (NT * G + 1) / 2;
+      uint32_t offs[2][NW];  // packed u16 source offsets, entry e = n*G + g
+#pragma unroll
+      for (int t = 0; t < 2; ++t) {
+#pragma unroll
+        for (int w = 0; w < NW; ++w) offs[t][w] = 0;
+#pragma unroll
+        for (int n = 0; n < NT; ++n) {
+          const int j = jb + 8 * n, hb = j / DG, jj = j % DG;
+#pragma unroll
+          for (int g = 0; g < G; ++g) {
+            const int e = n * G + g;
+            const uint32_t o = (uint32_t)perm_s[(t * HB + hb) * D + jj * G + g] * (BN * 2) + ch * 16;
+            offs[t][e >> 1] |= o << (16 * (e & 1));
+          }
+        }
+      }
+      const uint32_t dbase = (uint32_t)((ch >> 3) * (C::DR * 128) + jb * 128 + (((ch & 7) ^ jb) << 4));
+      for (int i = 0; i < nk; ++i) {
+        const int s = i % NS;
+        mbar_wait(&bars[B_KFULL + s], (i / NS) & 1);
+        const uint8_t* kt = sK + s * C::K_BYTES;
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          if (i >= nkt_t[t]) continue;
+          const int st = i % NKH;
+          mbar_wait(&bars[B_KHEMPTY + 2 * t + st], ((i / NKH) & 1) ^ 1);
+          uint8_t* kh = sKh + (t * NKH + st) * C::KH_BYTES + dbase;
+#pragma unroll
+          for (int n = 0; n < NT; ++n) {
+            uint32_t src[G];
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+              const int e = n * G + g;
+              src[g] = (offs[t][e >> 1] >> (16 * (e & 1))) & 0xFFFFu;
+            }
+            uint4 o;
+            if (G == 1) {
+              o = *reinterpret_cast<const uint4*>(kt + src[0]);
+            } else if (G == 2) {
+              // one RN rounding of the exact sum == RN(fp32 sum) for two bf16 operands
+              const uint4 x = *reinterpret_cast<const uint4*>(kt + src[0]);
+              const uint4 y = *reinterpret_cast<const uint4*>(kt + src[G - 1]);
+              o = make_uint4(hadd2_bf16(x.x, y.x), hadd2_bf16(x.y, y.y), hadd2_bf16(x.z, y.z), hadd2_bf16(x.w, y.w));
+            } else {
+              float acc[8];
+#pragma unroll
+              for (int e = 0; e < 8; ++e) acc[e] = 0.0f;
+#pragma unroll
+              for (int g = 0; g < G; ++g) {
+                const uint4 x = *reinterpret_cast<const uint4*>(kt + src[g]);
+                const uint32_t xv[4] = {x.x, x.y, x.z, x.w};
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                  const float2 fv = unpack_bf16x2(xv[e]);
+                  acc[2 * e] += fv.x;
+                  acc[2 * e + 1] += fv.y;
+                }
+              }
+              o = make_uint4(pack_bf16x2(acc[0], acc[1]), pack_bf16x2(acc[2], acc[3]), pack_bf16x2(acc[4], acc[5]),
+                             pack_bf16x2(acc[6], acc[7]));
+            }
+            *reinterpret_cast<uint4*>(kh + n * 1024) = o;
+          }
+          fence_proxy_async_smem();
+          mbar_arrive(&bars[B_KHFULL + 2 * t + st]);
+        }
+        mbar_arrive(&bars[B_KEMPTY + s]);
+      }
+    }
   }
 
   tc_fence_before();
@@ -401,14 +490,14 @@ __global__ void __launch_bounds__(kThreads, 1)
   }
 }
 
-template <int D, bool DISTR, int G, int HB>
+template <int D, bool DISTR, int G, int HB, int EMU>
 cudaError_t launch_one(const AttnLaunch& L, const AttnArgs& a, cudaStream_t st) {
   using C = Cfg<D, DISTR, G, HB>;
-  auto kern = attn_kernel<D, DISTR, G, HB>;
+  auto kern = attn_kernel<D, DISTR, G, HB, EMU>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
   if (e != cudaSuccess) return e;
-  dim3 grid(a.nqt, L.BH);
-  kern<<<grid, kThreads, C::SMEM, st>>>(*L.tmA, *L.tmK, *L.tmV, a);
+  dim3 grid((a.nqt + 1) / 2, L.BH);
+  kern<<<grid, threads_of<DISTR>(), C::SMEM, st>>>(*L.tmA, *L.tmK, *L.tmV, a);
   return cudaGetLastError();
 }
 
@@ -446,7 +535,15 @@ size_t attn_smem_bytes(int d, int G, int HB, int distr) {
 
 cudaError_t launch_attn(const AttnLaunch& L, const AttnArgs& a, cudaStream_t st) {
   const int d = L.d, G = L.G, HB = L.HB, distr = L.distr;
-#define DA_LAUNCH(D_, DI_, G_, HB_) return launch_one<D_, DI_, G_, HB_>(L, a, st)
+  // EMU (pairs of 8 on the FMA pipe): default per flavour, overridable for tuning (DA_EMU env).
+  const int emu = L.emu;
+#define DA_LAUNCH(D_, DI_, G_, HB_)                                                \
+  switch (emu) {                                                                   \
+    case 0: return launch_one<D_, DI_, G_, HB_, 0>(L, a, st);                      \
+    case 2: return launch_one<D_, DI_, G_, HB_, 2>(L, a, st);                      \
+    case 3: return launch_one<D_, DI_, G_, HB_, 3>(L, a, st);                      \
+    default: return launch_one<D_, DI_, G_, HB_, 4>(L, a, st);                     \
+  }
   DA_DISPATCH(DA_LAUNCH)
 #undef DA_LAUNCH
   return cudaErrorInvalidValue;

@@ -45,6 +45,7 @@ struct AttnLaunch {
   const CUtensorMap* tmA;  // Q (exact) or Q̂ (distr)
   const CUtensorMap* tmK;  // K natural (exact) or K^T (distr)
   const CUtensorMap* tmV;
+  int emu;                 // exp2 pairs (of 8) evaluated on the FMA pipe: 0, 2, 3 or 4
 };
 cudaError_t launch_attn(const AttnLaunch& L, const AttnArgs& a, cudaStream_t st);
 // Shared memory bytes the attention kernel uses (0 if unsupported combination).

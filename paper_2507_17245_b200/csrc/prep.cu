@@ -58,8 +58,8 @@ DA_DEV void hash_cta(const PrepArgs& a, int it, uint8_t* smem) {
   const int bh = it / a.nqb, qb = it % a.nqb;
   const int r0 = qb * a.block_l;
   const int rows = min(a.block_l, a.N - r0);
-  T* q_s = reinterpret_cast<T*>(smem);                                   // [rows][D]
-  float* proj_t = reinterpret_cast<float*>(smem + kMaxL * kMaxD * 4);    // [r][16]
+  T* q_s = reinterpret_cast<T*>(smem);                                          // [rows][D]
+  float* proj_t = reinterpret_cast<float*>(smem + kMaxL * kMaxD * sizeof(T));   // [r][16]
   uint32_t* pat_s = reinterpret_cast<uint32_t*>(proj_t + kMaxL * 16);    // [4][D]
   uint32_t* key_s = pat_s + 4 * kMaxD;                                   // [D]
   uint8_t* perm_s = reinterpret_cast<uint8_t*>(key_s + kMaxD);           // [D]
@@ -159,22 +159,38 @@ DA_DEV void hash_cta(const PrepArgs& a, int it, uint8_t* smem) {
   }
 }
 
-// K [N][d] -> K^T [d][N_pad] for one (bhkv, 64-key tile).
+// K [N][d] -> K^T [d][N_pad] for one (bhkv, 64-key tile). The smem tile row pitch is d+2
+// elements (65 words for d=128) so that the transposed reads (8 key rows x 4 columns per warp)
+// hit 16 distinct banks; global reads are 16-byte vectors, global writes 128-byte row segments.
 template <typename T>
 DA_DEV void kt_cta(const PrepArgs& a, int it, uint8_t* smem) {
   const int D = a.d;
   const int ntile = (a.N + 63) / 64;
   const int bhkv = it / ntile, t0 = (it % ntile) * 64;
   const int nkeys = min(64, a.N - t0);
-  uint16_t* tile = reinterpret_cast<uint16_t*>(smem);  // [64][D + 8] bf16
-  const int ld = D + 8;
+  uint16_t* tile = reinterpret_cast<uint16_t*>(smem);  // [64][D + 2] bf16
+  const int ld = D + 2;
   const T* kg = reinterpret_cast<const T*>(a.k) + ((size_t)bhkv * a.N + t0) * D;
-  for (int i = threadIdx.x; i < 64 * D; i += kThreads) {
-    const int t = i / D, c = i % D;
-    tile[t * ld + c] = (t < nkeys) ? f2bf(load_f<T>(kg + (size_t)t * D + c)) : (uint16_t)0;
+  constexpr int VEC = 16 / sizeof(T);
+  const int vpr = D / VEC;  // 16-byte vectors per K row
+  for (int i = threadIdx.x; i < 64 * vpr; i += kThreads) {
+    const int t = i / vpr, cv = i % vpr;
+    uint32_t w[4] = {0u, 0u, 0u, 0u};
+    if (t < nkeys) {
+      const uint4 x = *reinterpret_cast<const uint4*>(kg + (size_t)t * D + cv * VEC);
+      if (sizeof(T) == 2) {
+        w[0] = x.x; w[1] = x.y; w[2] = x.z; w[3] = x.w;
+      } else {
+        w[0] = (uint32_t)f2bf(__uint_as_float(x.x)) | ((uint32_t)f2bf(__uint_as_float(x.y)) << 16);
+        w[1] = (uint32_t)f2bf(__uint_as_float(x.z)) | ((uint32_t)f2bf(__uint_as_float(x.w)) << 16);
+      }
+    }
+    uint32_t* dst = reinterpret_cast<uint32_t*>(tile + t * ld + cv * VEC);
+#pragma unroll
+    for (int e = 0; e < VEC / 2; ++e) dst[e] = w[e];
   }
   __syncthreads();
-  // Each thread writes one 16-byte chunk: 8 consecutive keys of one K^T row.
+  // Each thread writes one 16-byte chunk: 8 consecutive keys of one K^T row (8 lanes = 128 B).
   uint16_t* ktg = a.kt + (size_t)bhkv * D * a.N_pad;
   for (int i = threadIdx.x; i < D * 8; i += kThreads) {
     const int c = i / 8, ch = i % 8;
@@ -206,9 +222,8 @@ __global__ void convert_kernel(const float* __restrict__ src, uint16_t* __restri
 }  // namespace
 
 size_t prep_smem_bytes(int in_f32) {
-  const size_t q = (size_t)kMaxL * kMaxD * 4;  // room for f32 too
+  const size_t q = (size_t)kMaxL * kMaxD * (in_f32 ? 4 : 2);
   return q + kMaxL * 16 * 4 + 4 * kMaxD * 4 + kMaxD * 4 + kMaxD + 16;
-  (void)in_f32;
 }
 
 cudaError_t launch_prep(const PrepArgs& a, cudaStream_t st) {

@@ -172,6 +172,43 @@ DA_DEV float2 fma2(float2 a, float2 b, float2 c) {
   asm("mov.b64 {%0, %1}, %2;" : "=f"(d.x), "=f"(d.y) : "l"(rd));
   return d;
 }
+DA_DEV float2 fadd2(float2 a, float2 b) {
+  uint64_t ra, rb, rd;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(ra) : "f"(a.x), "f"(a.y));
+  asm("mov.b64 %0, {%1, %2};" : "=l"(rb) : "f"(b.x), "f"(b.y));
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(rd) : "l"(ra), "l"(rb));
+  float2 d;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(d.x), "=f"(d.y) : "l"(rd));
+  return d;
+}
+// Three-input max (SASS FMNMX3).
+DA_DEV float max3(float a, float b, float c) {
+  float d;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
+  return d;
+}
+// bf16x2 add with one round-to-nearest-even (equal to rounding the exact fp32 sum of two bf16).
+DA_DEV uint32_t hadd2_bf16(uint32_t a, uint32_t b) {
+  uint32_t d;
+  asm("add.rn.bf16x2 %0, %1, %2;" : "=r"(d) : "r"(a), "r"(b));
+  return d;
+}
+// 2^x for a pair on the FMA pipe (no MUFU): Cody-Waite split x = j + f, |f| <= 1/2, degree-3
+// polynomial for 2^f (max rel. error 7.5e-5, below the bf16 rounding of P), exponent add by an
+// integer multiply-add. x is clamped to >= -125 (2^-125 stands in for 0 for masked scores).
+DA_DEV float2 exp2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -125.0f);
+  x.y = fmaxf(x.y, -125.0f);
+  const float2 magic = make_float2(12582912.0f, 12582912.0f);  // 1.5 * 2^23: round to integer
+  const float2 t = fadd2(x, magic);
+  const float2 r = fadd2(t, make_float2(-12582912.0f, -12582912.0f));
+  const float2 f = fma2(r, make_float2(-1.0f, -1.0f), x);
+  float2 p = fma2(f, make_float2(0.055171456f, 0.055171456f), make_float2(0.24261115f, 0.24261115f));
+  p = fma2(p, f, make_float2(0.69326103f, 0.69326103f));
+  p = fma2(p, f, make_float2(0.99992806f, 0.99992806f));
+  return make_float2(__uint_as_float(__float_as_uint(t.x) * 8388608u + __float_as_uint(p.x)),
+                     __uint_as_float(__float_as_uint(t.y) * 8388608u + __float_as_uint(p.y)));
+}
 DA_DEV uint32_t pack_bf16x2(float lo, float hi) {
   uint32_t r;
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
