@@ -20,7 +20,7 @@ EXPORTED = (
     "distr_attn_init_params", "distr_attn_fwd", "distr_attn_fwd_ex", "distr_attn_fwd_host",
     "exact_attn_fwd_ex", "distr_attn_hash", "distr_attn_projection", "distr_attn_workspace_size",
     "distr_attn_status_string", "distr_attn_last_error", "distr_attn_last_launch_count",
-    "distr_attn_set_profile_events",
+    "distr_attn_set_profile_events", "distr_attn_set_trace",
 )
 
 
@@ -70,6 +70,7 @@ def lib() -> ctypes.CDLL:
             L.distr_attn_last_error.restype = ctypes.c_char_p
             L.distr_attn_last_launch_count.restype = i32
             L.distr_attn_set_profile_events.argtypes = [vp, vp, vp]
+            L.distr_attn_set_trace.argtypes = [vp]
             _lib = L
     return _lib
 

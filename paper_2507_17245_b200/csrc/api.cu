@@ -23,6 +23,7 @@ namespace {
 thread_local std::string g_last_error;
 thread_local int g_last_launches = 0;
 thread_local cudaEvent_t g_ev[3] = {nullptr, nullptr, nullptr};
+thread_local long long* g_trace = nullptr;
 
 void record_ev(int i, cudaStream_t st) {
   if (g_ev[i]) cudaEventRecord(g_ev[i], st);
@@ -319,6 +320,8 @@ int forward(const void* q, const void* k, const void* v, void* out, const da_par
   aa.out = out;
   aa.out_f32 = P.f32;
   aa.lse = p->lse;
+  aa.trace = g_trace;
+  g_trace = nullptr;
   da::AttnLaunch L{P.d, P.G, P.HB, distr ? 1 : 0, (int)BH, &tmA, &tmK, &tmV, default_emu(P, distr)};
   record_ev(1, st);
   DA_CUDA(da::launch_attn(L, aa, st));
@@ -447,6 +450,11 @@ const char* distr_attn_status_string(int status) {
 const char* distr_attn_last_error(void) { return g_last_error.c_str(); }
 
 int distr_attn_last_launch_count(void) { return g_last_launches; }
+
+int distr_attn_set_trace(void* device_buf) {
+  g_trace = static_cast<long long*>(device_buf);
+  return DA_OK;
+}
 
 int distr_attn_set_profile_events(void* ev_start, void* ev_attn, void* ev_end) {
   g_ev[0] = static_cast<cudaEvent_t>(ev_start);

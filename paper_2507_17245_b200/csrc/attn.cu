@@ -4,7 +4,7 @@
 // iterations per CTA); the inner loop walks 128-key tiles that both Q tiles share in smem.
 // Warp roles (384 threads):
 //   warp 0      TMA producer: Q (exact) or Q̂ (distr) of both tiles once, then K (exact) or K^T
-//               (distr) and V tiles through an NS-stage mbarrier ring.
+//               (distr) tiles through an NS-stage mbarrier ring; warp 2: the V ring.
 //   warp 1      TMEM allocator + single-thread tcgen05.mma issuer, ping-ponging the two tiles:
 //                 S_t  = A_t · B_t^T        (M=128, N=128, K = d or DR = HB*d/G*; fp32 in TMEM)
 //                 O_t += P_t · V            (A = P_t bf16 read from TMEM, B = V MN-major, N = d)
@@ -108,6 +108,9 @@ __global__ void __launch_bounds__(threads_of<DISTR>(), 1)
 
   const int warp = warp_id(), lane = lane_id();
   const int bh = blockIdx.y;
+  long long* const trace = (args.trace && blockIdx.x == 0 && blockIdx.y == 0) ? args.trace : nullptr;
+#define DA_TRACE(slot, idx, cond) \
+  if (trace && (cond)) trace[(slot) * 256 + ((idx) & 255)] = clock64();
   // causal: heaviest pairs of Q tiles first
   const int pair = args.causal ? ((args.nqt + 1) / 2 - 1 - (int)blockIdx.x) : (int)blockIdx.x;
   const int b = bh / args.H, h = bh % args.H;
@@ -182,6 +185,8 @@ __global__ void __launch_bounds__(threads_of<DISTR>(), 1)
         for (int bx = 0; bx < C::A_NBOX; ++bx)
           tma_load_3d(sA + t * C::A_BYTES + bx * C::A_BOX_BYTES, &tmA, &bars[B_Q], bx * C::A_BOX_COLS,
                       (qt0 + t) * BM, bh);
+      // K (or K^T) ring; V has its own producer (warp 2) so K prefetch never waits behind the
+      // PV that frees a V stage.
       for (int i = 0; i < nk; ++i) {
         const int s = i % NS;
         const uint32_t ph = (i / NS) & 1;
@@ -193,6 +198,14 @@ __global__ void __launch_bounds__(threads_of<DISTR>(), 1)
           for (int bx = 0; bx < D / 64; ++bx)
             tma_load_3d(sK + s * C::K_BYTES + bx * (BN * 128), &tmK, &bars[B_KFULL + s], bx * 64, i * BN, bhkv);
         }
+      }
+    }
+  } else if (warp == 2) {
+    // ------------------------------------------------------------------ TMA producer (V ring)
+    if (lane == 0) {
+      for (int i = 0; i < nk; ++i) {
+        const int s = i % NS;
+        const uint32_t ph = (i / NS) & 1;
         mbar_wait(&bars[B_VEMPTY + s], ph ^ 1);
         mbar_arrive_expect_tx(&bars[B_VFULL + s], C::V_BYTES);
         for (int bx = 0; bx < D / 64; ++bx)
@@ -231,10 +244,12 @@ __global__ void __launch_bounds__(threads_of<DISTR>(), 1)
         }
         mma_commit(&bars[B_SFULL + t]);
         if (DISTR) mma_commit(&bars[B_KHEMPTY + 2 * t + i % NKH]);
+        DA_TRACE(6 + t, i, true);
       };
       auto issue_pv = [&](int t, int j) {
         const int s = j % NS;
         mbar_wait(&bars[B_PFULL + t], j & 1);
+        DA_TRACE(8 + t, j, true);
         if (t == 0 || nkt_t[0] <= j) mbar_wait(&bars[B_VFULL + s], (j / NS) & 1);
         tc_fence_after();
         const uint32_t v_base = smem_u32(sV + s * C::V_BYTES);
@@ -271,7 +286,7 @@ __global__ void __launch_bounds__(threads_of<DISTR>(), 1)
       if (nk - 1 < nkt_t[1]) issue_pv(1, nk - 1);
       release_v(nk - 1);
     }
-  }  // warps 2-3 idle
+  }  // warp 3 idle
   } else if (warp < 12) {
     if (DISTR)
       asm volatile("setmaxnreg.inc.sync.aligned.u32 184;");
@@ -290,7 +305,9 @@ __global__ void __launch_bounds__(threads_of<DISTR>(), 1)
     float m = -INFINITY;  // running max of scaled log2 scores (possibly stale by <= 8)
     float l = 0.0f;
     for (int i = 0; i < nkt; ++i) {
+      DA_TRACE(13 + t, i, row == 0);
       mbar_wait(&bars[B_SFULL + t], i & 1);
+      DA_TRACE(3 * t, i, row == 0);
       tc_fence_after();
       uint32_t sr[BN];
 #pragma unroll
@@ -317,6 +334,7 @@ __global__ void __launch_bounds__(threads_of<DISTR>(), 1)
         for (int j = 0; j < 8; ++j) mx8[j] = max3(mx8[j], s[e + j], s[e + 8 + j]);
       const float mx = max3(max3(mx8[0], mx8[1], mx8[2]), max3(mx8[3], mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]));
       const float mnew = fmaxf(m, mx * sl2);
+      DA_TRACE(3 * t + 1, i, row == 0);
       if (i == 0) {
         m = mnew;
       } else {
@@ -365,6 +383,7 @@ __global__ void __launch_bounds__(threads_of<DISTR>(), 1)
       tmem_st_wait();
       tc_fence_before();
       mbar_arrive(&bars[B_PFULL + t]);
+      DA_TRACE(3 * t + 2, i, row == 0);
     }
     if (nkt > 0) {
       mbar_wait(&bars[B_OFULL + t], 0);
@@ -431,6 +450,7 @@ __global__ void __launch_bounds__(threads_of<DISTR>(), 1)
       for (int i = 0; i < nk; ++i) {
         const int s = i % NS;
         mbar_wait(&bars[B_KFULL + s], (i / NS) & 1);
+        DA_TRACE(10, i, f == 0);
         const uint8_t* kt = sK + s * C::K_BYTES;
 #pragma unroll
         for (int t = 0; t < 2; ++t) {
@@ -476,6 +496,7 @@ __global__ void __launch_bounds__(threads_of<DISTR>(), 1)
           }
           fence_proxy_async_smem();
           mbar_arrive(&bars[B_KHFULL + 2 * t + st]);
+          DA_TRACE(11 + t, i, f == 0);
         }
         mbar_arrive(&bars[B_KEMPTY + s]);
       }
