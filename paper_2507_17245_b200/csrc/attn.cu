@@ -53,7 +53,7 @@ struct Cfg {
   static constexpr int KH_BYTES = DISTR ? DR * BN * 2 : 0;
   static constexpr int al(int x) { return (x + 1023) / 1024 * 1024; }
   static constexpr int bytes(int ns, int nkh) {
-    return al(2 * A_BYTES) + ns * (K_BYTES + V_BYTES) + 2 * nkh * KH_BYTES + 1024;
+    return al(2 * A_BYTES) + ns * (K_BYTES + V_BYTES) + 2 * nkh * KH_BYTES + 1024 + 6144;
   }
   // Deepest K/V ring (NS) and K̂ ring (NKH) that fit the 227 KB of shared memory.
   static constexpr int NKH = !DISTR ? 0 : (bytes(2, 2) <= kSmemMax ? 2 : 1);
@@ -64,7 +64,7 @@ struct Cfg {
   static constexpr int OFF_KH = OFF_V + NS * V_BYTES;
   static constexpr int OFF_PERM = OFF_KH + 2 * NKH * KH_BYTES;
   static constexpr int OFF_BAR = OFF_PERM + 2 * 2 * 128;
-  static constexpr int SMEM = OFF_BAR + 512 + 1024;  // + slack for 1024-B alignment
+  static constexpr int SMEM = OFF_BAR + 256 + 6144 + 1024;  // barriers, row-max/sum exchange, align slack
   static constexpr uint32_t A_LAYOUT = A_SW == 128 ? kSw128 : (A_SW == 64 ? kSw64 : kSw32);
   static_assert(DR % 16 == 0 && DR >= 16 && DR <= 128, "reduced width");
   static_assert(A_COLS % A_BOX_COLS == 0, "A boxes");
@@ -139,7 +139,7 @@ __global__ void __launch_bounds__(threads_of<DISTR>(), 1)
         mbar_init(&bars[B_KHEMPTY + 2 * t + st], 1);
       }
       mbar_init(&bars[B_SFULL + t], 1);
-      mbar_init(&bars[B_PFULL + t], 128);
+      mbar_init(&bars[B_PFULL + t], 256);
       mbar_init(&bars[B_OFULL + t], 1);
     }
     fence_mbar_init();
@@ -163,11 +163,11 @@ __global__ void __launch_bounds__(threads_of<DISTR>(), 1)
   tc_fence_after();
   const uint32_t tmem = *tmem_ptr_s;
 
-  // Register split: the TMA/MMA warpgroup (and the fusion warpgroup) hand registers to the two
-  // softmax warpgroups. exact: 128*88 + 256*208 = 384*168; distr: 128*48 + 128*96 + 256*184 <=
-  // 512*128 — never more than the pool the launch reserved (an .inc that exceeds what the .dec
-  // calls released would block forever). Each setmaxnreg sits at the head of its warpgroup's
-  // branch so ptxas budgets each region separately.
+  // Register split (distr, 512 threads at 128 registers): the TMA/MMA warpgroup gives 64 of its
+  // registers to the softmax warpgroups (128*64 + 256*160 + 128*128 = 512*128; an .inc that
+  // exceeds what the .dec released would block forever). The exact kernel (384 threads at 168)
+  // needs no split. Each setmaxnreg sits at the head of its warpgroup's branch so ptxas budgets
+  // each region separately.
   if (warp < 4) {
   if (DISTR)
     asm volatile("setmaxnreg.dec.sync.aligned.u32 48;");
@@ -289,85 +289,97 @@ __global__ void __launch_bounds__(threads_of<DISTR>(), 1)
   }  // warp 3 idle
   } else if (warp < 12) {
     if (DISTR)
-      asm volatile("setmaxnreg.inc.sync.aligned.u32 184;");
-    else
-      asm volatile("setmaxnreg.inc.sync.aligned.u32 208;");
+      asm volatile("setmaxnreg.inc.sync.aligned.u32 160;");
     // ------------------------------------------------------------------ softmax (warps 4..11)
-    const int t = (warp - 4) >> 2;  // Q tile of this warpgroup
-    const int nkt = nkt_t[t];
-    const int row = (warp & 3) * 32 + lane;
-    const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
-    const uint32_t tS = tmem + lane_base + kColS + 128u * t;
-    const uint32_t tO = tmem + lane_base + (uint32_t)(t * D);
-    const int q0 = (qt0 + t) * BM;
-    const int q_row = q0 + row;
+    // All 8 softmax warps work on ONE Q tile at a time, alternating tiles (t = 0, 1, 0, 1, ...)
+    // in the MMA's issue order. Warps w and w+4 own the same 32 TMEM lanes (rows) and split the
+    // 128 key columns: half = (w - 4) / 4 takes columns [64*half, 64*half + 64). The row max is
+    // combined through shared memory with a 64-thread named barrier per warp pair; the running
+    // max m is therefore identical in both halves, so each half keeps its own partial row sum and
+    // rescales its own half of O's columns; the halves' sums are combined once, at the end.
+    // While these warps run tile t's exp phase the tensor core computes the other tile.
+    const int half = (warp - 4) >> 2;
+    const int quad = warp & 3;
+    const int row = quad * 32 + lane;
+    const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
+    float* xmax = reinterpret_cast<float*>(bars + B_COUNT);  // max [2 parity][2 t][2 half][128], sums [2 t][2 half][128]
     const float sl2 = args.scale_log2;
-    float m = -INFINITY;  // running max of scaled log2 scores (possibly stale by <= 8)
-    float l = 0.0f;
-    for (int i = 0; i < nkt; ++i) {
-      DA_TRACE(13 + t, i, row == 0);
-      mbar_wait(&bars[B_SFULL + t], i & 1);
-      DA_TRACE(3 * t, i, row == 0);
-      tc_fence_after();
-      uint32_t sr[BN];
+    float m[2] = {-INFINITY, -INFINITY};  // running max per tile (scaled log2; stale by <= 8)
+    float l[2] = {0.0f, 0.0f};            // this half's partial row sums
+    auto pair_sync = [&]() {  // warps quad+4 and quad+8 (same rows, both halves)
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + quad) : "memory");
+    };
+    for (int i = 0; i < nk; ++i) {
 #pragma unroll
-      for (int c = 0; c < BN / 32; ++c)
-        tmem_ld32(tS + 32u * c, *reinterpret_cast<uint32_t(*)[32]>(&sr[32 * c]));
-      tmem_ld_wait();
-      float s[BN];
+      for (int t = 0; t < 2; ++t) {
+        if (i >= nkt_t[t]) continue;
+        const uint32_t tS = tmem + lane_base + kColS + 128u * t + 64u * half;
+        const uint32_t tO = tmem + lane_base + (uint32_t)(t * D) + (uint32_t)(half * (D / 2));
+        const int q0 = (qt0 + t) * BM;
+        const int q_row = q0 + row;
+        DA_TRACE(13 + t, i, row == 0 && half == 0);
+        mbar_wait(&bars[B_SFULL + t], i & 1);
+        DA_TRACE(3 * t, i, row == 0 && half == 0);
+        tc_fence_after();
+        uint32_t sr[64];
+        tmem_ld32(tS, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
+        tmem_ld32(tS + 32u, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
+        tmem_ld_wait();
+        float sv[64];
 #pragma unroll
-      for (int e = 0; e < BN; ++e) s[e] = __uint_as_float(sr[e]);
-      const int kbase = i * BN;
-      if (kbase + BN > args.N || (args.causal && kbase + BN - 1 > q0)) {
-        const int lim = args.causal ? min(args.N - 1, q_row) : args.N - 1;
+        for (int e = 0; e < 64; ++e) sv[e] = __uint_as_float(sr[e]);
+        const int kbase = i * BN + 64 * half;
+        if (kbase + 64 > args.N || (args.causal && kbase + 63 > q0)) {
+          const int lim = args.causal ? min(args.N - 1, q_row) : args.N - 1;
 #pragma unroll
-        for (int e = 0; e < BN; ++e)
-          if (kbase + e > lim) s[e] = -INFINITY;
-      }
-      // Row max: 8 independent FMNMX3 chains (depth 8) instead of one 128-long chain.
-      float mx8[8];
+          for (int e = 0; e < 64; ++e)
+            if (kbase + e > lim) sv[e] = -INFINITY;
+        }
+        // Row max over this half: 8 independent FMNMX3 chains; then combine the two halves.
+        float mx8[8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) mx8[j] = max3(s[j], s[8 + j], s[120 + j]);
+        for (int j = 0; j < 8; ++j) mx8[j] = max3(sv[j], sv[8 + j], sv[56 + j]);
 #pragma unroll
-      for (int e = 16; e < 120; e += 16)
+        for (int e = 16; e < 56; e += 16)
 #pragma unroll
-        for (int j = 0; j < 8; ++j) mx8[j] = max3(mx8[j], s[e + j], s[e + 8 + j]);
-      const float mx = max3(max3(mx8[0], mx8[1], mx8[2]), max3(mx8[3], mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]));
-      const float mnew = fmaxf(m, mx * sl2);
-      DA_TRACE(3 * t + 1, i, row == 0);
-      if (i == 0) {
-        m = mnew;
-      } else {
-        // S_t(i) was committed after PV_t(i-1) was issued, so O_t already holds sum_{<i} P V.
-        const bool need = mnew > m + 8.0f;
-        if (__any_sync(0xffffffffu, need)) {
-          const float f = need ? ex2(m - mnew) : 1.0f;
+          for (int j = 0; j < 8; ++j) mx8[j] = max3(mx8[j], sv[e + j], sv[e + 8 + j]);
+        float mx = max3(max3(mx8[0], mx8[1], mx8[2]), max3(mx8[3], mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]));
+        xmax[((i & 1) * 4 + t * 2 + half) * 128 + row] = mx;
+        pair_sync();
+        mx = fmaxf(mx, xmax[((i & 1) * 4 + t * 2 + (half ^ 1)) * 128 + row]);
+        const float mnew = fmaxf(m[t], mx * sl2);
+        DA_TRACE(3 * t + 1, i, row == 0 && half == 0);
+        if (i == 0) {
+          m[t] = mnew;
+        } else {
+          // S_t(i) was committed after PV_t(i-1) was issued, so O_t holds sum_{<i} P V.
+          const bool need = mnew > m[t] + 8.0f;
+          if (__any_sync(0xffffffffu, need)) {
+            const float f = need ? ex2(m[t] - mnew) : 1.0f;
 #pragma unroll
-          for (int c = 0; c < D / 32; ++c) {
-            uint32_t r[32];
-            tmem_ld32(tO + 32u * c, r);
-            tmem_ld_wait();
+            for (int c = 0; c < D / 64; ++c) {
+              uint32_t r[32];
+              tmem_ld32(tO + 32u * c, r);
+              tmem_ld_wait();
 #pragma unroll
-            for (int e = 0; e < 32; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * f);
-            tmem_st32(tO + 32u * c, r);
-          }
-          if (need) {
-            l *= f;
-            m = mnew;
+              for (int e = 0; e < 32; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * f);
+              tmem_st32(tO + 32u * c, r);
+            }
+            if (need) {
+              l[t] *= f;
+              m[t] = mnew;
+            }
           }
         }
-      }
-      // p = 2^(s*scale*log2e - m): FFMA2 for the affine part, EMU/8 of the pairs on the FMA pipe,
-      // the rest on MUFU; 4 independent FADD2 partial sums.
-      const float2 sl2x2 = make_float2(sl2, sl2), nm2 = make_float2(-m, -m);
-      float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f)};
-#pragma unroll
-      for (int c = 0; c < 2; ++c) {
+        // p = 2^(s*scale*log2e - m): FFMA2 for the affine part, EMU/8 of the pairs on the FMA
+        // pipe, the rest on MUFU; 4 independent FADD2 partial sums.
+        const float2 sl2x2 = make_float2(sl2, sl2), nm2 = make_float2(-m[t], -m[t]);
+        float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                         make_float2(0.f, 0.f)};
         uint32_t pr[32];
 #pragma unroll
         for (int e = 0; e < 32; ++e) {
-          const int col = 64 * c + 2 * e;
-          const float2 x = fma2(make_float2(s[col], s[col + 1]), sl2x2, nm2);
+          const float2 x = fma2(make_float2(sv[2 * e], sv[2 * e + 1]), sl2x2, nm2);
           float2 p;
           if ((e & 7) >= 8 - EMU)
             p = exp2_poly2(x);
@@ -376,26 +388,35 @@ __global__ void __launch_bounds__(threads_of<DISTR>(), 1)
           acc[e & 3] = fadd2(acc[e & 3], p);
           pr[e] = pack_bf16x2(p.x, p.y);
         }
-        tmem_st32(tS + 32u * c, pr);
+        // P of keys [64*half, 64*half + 64) -> columns [32*half, 32*half + 32) of S_t
+        tmem_st32(tmem + lane_base + kColS + 128u * t + 32u * half, pr);
+        const float2 a = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
+        l[t] += a.x + a.y;
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&bars[B_PFULL + t]);
+        DA_TRACE(3 * t + 2, i, row == 0 && half == 0);
       }
-      const float2 a = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
-      l += a.x + a.y;
-      tmem_st_wait();
-      tc_fence_before();
-      mbar_arrive(&bars[B_PFULL + t]);
-      DA_TRACE(3 * t + 2, i, row == 0);
     }
-    if (nkt > 0) {
+    // Epilogue: both halves' row sums, each half writes its d/2 output columns.
+#pragma unroll
+    for (int t = 0; t < 2; ++t) {
+      if (nkt_t[t] == 0) continue;
+      const int q_row = (qt0 + t) * BM + row;
+      const uint32_t tO = tmem + lane_base + (uint32_t)(t * D) + (uint32_t)(half * (D / 2));
+      xmax[1024 + (t * 2 + half) * 128 + row] = l[t];
+      pair_sync();
+      const float lt = l[t] + xmax[1024 + (t * 2 + (half ^ 1)) * 128 + row];
       mbar_wait(&bars[B_OFULL + t], 0);
       tc_fence_after();
-      const float inv = 1.0f / l;
+      const float inv = 1.0f / lt;
 #pragma unroll
-      for (int c = 0; c < D / 32; ++c) {
+      for (int c = 0; c < D / 64; ++c) {
         uint32_t r[32];
         tmem_ld32(tO + 32u * c, r);
         tmem_ld_wait();
         if (q_row < args.N) {
-          const size_t off = ((size_t)bh * args.N + q_row) * D + 32 * c;
+          const size_t off = ((size_t)bh * args.N + q_row) * D + half * (D / 2) + 32 * c;
           if (args.out_f32) {
             float4* o = reinterpret_cast<float4*>(static_cast<float*>(args.out) + off);
 #pragma unroll
@@ -413,11 +434,10 @@ __global__ void __launch_bounds__(threads_of<DISTR>(), 1)
           }
         }
       }
-      if (args.lse && q_row < args.N)
-        args.lse[(size_t)bh * args.N + q_row] = (m + log2f(l)) * 0.69314718055994531f;
+      if (args.lse && q_row < args.N && half == 0)
+        args.lse[(size_t)bh * args.N + q_row] = (m[t] + log2f(lt)) * 0.69314718055994531f;
     }
   } else {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 96;");
     // ------------------------------------------------------------------ fusion (warps 12..15)
     // Thread f owns 16-byte chunk ch = f % 16 (8 keys) of K̂^T rows j = f/16 + 8n, n < DR/8.
     // Its source-row byte offsets (perm rows * 256 + ch * 16) are fixed for the CTA's lifetime,
