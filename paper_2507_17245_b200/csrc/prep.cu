@@ -9,7 +9,7 @@
 //   kernel's TMA reads: [BH][N][DR], DR = HB * d / G, hash block hb of a 128-row tile occupying
 //   columns [hb*d/G, (hb+1)*d/G) and zeros elsewhere (block-diagonal stacking for block_l = 64).
 // K^T CTAs, one per (b*H_kv + h, 64-key tile): K [N][d] -> K^T [d][N_pad] (bf16), the layout
-//   in which per-(Q block, K tile) fusion is a sum of whole 16-byte row chunks (DESIGN.md §5).
+//   in which per-(Q block, K tile) fusion is a sum of whole 16-byte row chunks (DESIGN.md §6.1).
 //
 // Bit-exactness contract with oracle/oracle.c: same fp32 operations in the same order, strict
 // y > 0, LSB = projection row 0, ties broken by column index. No fast-math in this file.
@@ -26,7 +26,6 @@ namespace {
 
 constexpr int kThreads = 256;
 constexpr int kMaxL = 128;
-constexpr int kMaxD = 128;
 
 template <typename T>
 DA_DEV float load_f(const T* p);
@@ -51,73 +50,83 @@ DA_DEV uint32_t inverse_gray16(uint32_t p) {
   return p & 0xFFFFu;
 }
 
-// Number of 16-byte vectors per Q row.
-template <typename T>
+DA_DEV int ilog2(int x) { return 31 - __clz(x); }
+
+// Q block staging: row pitch D+8 elements (16-byte aligned rows) shifts consecutive rows by
+// 4 banks so the 2-byte Q̂ gathers of the 4 rows a warp covers spread over the banks.
+template <typename T, int D>
+constexpr int q_pitch() { return D + 16 / (int)sizeof(T); }
+
+template <typename T, int D>
 DA_DEV void hash_cta(const PrepArgs& a, int it, uint8_t* smem) {
-  const int D = a.d;
-  const int bh = it / a.nqb, qb = it % a.nqb;
+  constexpr int QP = q_pitch<T, D>();
+  constexpr int QBYTES = kMaxL * QP * (int)sizeof(T);
+  const int bh = it / a.nqb, qb = it - bh * a.nqb;
   const int r0 = qb * a.block_l;
   const int rows = min(a.block_l, a.N - r0);
-  T* q_s = reinterpret_cast<T*>(smem);                                          // [rows][D]
-  float* proj_t = reinterpret_cast<float*>(smem + kMaxL * kMaxD * sizeof(T));   // [r][16]
-  uint32_t* pat_s = reinterpret_cast<uint32_t*>(proj_t + kMaxL * 16);    // [4][D]
-  uint32_t* key_s = pat_s + 4 * kMaxD;                                   // [D]
-  uint8_t* perm_s = reinterpret_cast<uint8_t*>(key_s + kMaxD);           // [D]
+  const int lsh = ilog2(a.block_l);
+  T* q_s = reinterpret_cast<T*>(smem);                                 // [rows][QP]
+  float* proj_t = reinterpret_cast<float*>(smem + QBYTES);             // [r][16]
+  uint32_t* pat_s = reinterpret_cast<uint32_t*>(proj_t + kMaxL * 16);  // [NKG][D]
+  uint32_t* key_s = pat_s + 4 * D;                                     // [D]
+  uint8_t* perm_s = reinterpret_cast<uint8_t*>(key_s + D);             // [D]
 
-  // Stage the Q block (16-byte vectors, coalesced) and the transposed projection.
+  // Stage the Q block (16-byte global loads, coalesced) and the transposed projection [r][16].
   const T* qg = reinterpret_cast<const T*>(a.q) + ((size_t)bh * a.N + r0) * D;
-  const int vec = 16 / sizeof(T);
-  const int nvec = rows * D / vec;
-  for (int i = threadIdx.x; i < nvec; i += kThreads)
-    reinterpret_cast<uint4*>(q_s)[i] = reinterpret_cast<const uint4*>(qg)[i];
+  constexpr int VEC = 16 / sizeof(T);
+  constexpr int VPR = D / VEC;  // vectors per row
+  {
+    // all loads of a thread in flight before the first shared store
+    constexpr int NIT = kMaxL * VPR / kThreads;
+    uint4 v[NIT];
+#pragma unroll
+    for (int u = 0; u < NIT; ++u) {
+      const int i = threadIdx.x + u * kThreads;
+      if (i < rows * VPR) v[u] = reinterpret_cast<const uint4*>(qg)[i];
+    }
+#pragma unroll
+    for (int u = 0; u < NIT; ++u) {
+      const int i = threadIdx.x + u * kThreads;
+      if (i < rows * VPR) *reinterpret_cast<uint4*>(q_s + (i / VPR) * QP + (i % VPR) * VEC) = v[u];
+    }
+  }
   for (int i = threadIdx.x; i < 16 * a.block_l; i += kThreads) {
-    const int k = i / a.block_l, r = i % a.block_l;
+    const int k = i >> lsh, r = i & (a.block_l - 1);
     proj_t[r * 16 + k] = a.proj[i];
   }
   __syncthreads();
 
   // Projection: thread -> (column c, group of KPT consecutive projection rows).
-  const int nkg = kThreads / D;  // 2 (d=128) or 4 (d=64)
-  const int kpt = 16 / nkg;      // 8 or 4
+  constexpr int NKG = kThreads / D;  // 2 (d=128) or 4 (d=64)
+  constexpr int KPT = 16 / NKG;      // 8 or 4
   const int c = threadIdx.x % D, kg = threadIdx.x / D;
-  const int k0 = kg * kpt;
-  float2 y[4];
+  const int k0 = kg * KPT;
+  float2 y[KPT / 2];
 #pragma unroll
-  for (int m = 0; m < 4; ++m) y[m] = make_float2(0.0f, 0.0f);
-  if (kpt == 8) {
-    for (int r = 0; r < rows; ++r) {
-      const float qv = load_f<T>(q_s + r * D + c);
-      const float2 qq = make_float2(qv, qv);
-      const float4 pa = *reinterpret_cast<const float4*>(proj_t + r * 16 + k0);
-      const float4 pb = *reinterpret_cast<const float4*>(proj_t + r * 16 + k0 + 4);
-      y[0] = fma2(make_float2(pa.x, pa.y), qq, y[0]);
-      y[1] = fma2(make_float2(pa.z, pa.w), qq, y[1]);
-      y[2] = fma2(make_float2(pb.x, pb.y), qq, y[2]);
-      y[3] = fma2(make_float2(pb.z, pb.w), qq, y[3]);
-    }
-  } else {
-    for (int r = 0; r < rows; ++r) {
-      const float qv = load_f<T>(q_s + r * D + c);
-      const float2 qq = make_float2(qv, qv);
-      const float4 pa = *reinterpret_cast<const float4*>(proj_t + r * 16 + k0);
-      y[0] = fma2(make_float2(pa.x, pa.y), qq, y[0]);
-      y[1] = fma2(make_float2(pa.z, pa.w), qq, y[1]);
+  for (int m = 0; m < KPT / 2; ++m) y[m] = make_float2(0.0f, 0.0f);
+  for (int r = 0; r < rows; ++r) {
+    const float qv = load_f<T>(q_s + r * QP + c);
+    const float2 qq = make_float2(qv, qv);
+#pragma unroll
+    for (int m = 0; m < KPT / 4; ++m) {
+      const float4 pa = *reinterpret_cast<const float4*>(proj_t + r * 16 + k0 + 4 * m);
+      y[2 * m] = fma2(make_float2(pa.x, pa.y), qq, y[2 * m]);
+      y[2 * m + 1] = fma2(make_float2(pa.z, pa.w), qq, y[2 * m + 1]);
     }
   }
   uint32_t part = 0;
 #pragma unroll
-  for (int m = 0; m < 4; ++m) {
-    if (2 * m < kpt) {
-      part |= (y[m].x > 0.0f ? 1u : 0u) << (k0 + 2 * m);
-      part |= (y[m].y > 0.0f ? 1u : 0u) << (k0 + 2 * m + 1);
-    }
+  for (int m = 0; m < KPT / 2; ++m) {
+    part |= (y[m].x > 0.0f ? 1u : 0u) << (k0 + 2 * m);
+    part |= (y[m].y > 0.0f ? 1u : 0u) << (k0 + 2 * m + 1);
   }
-  pat_s[kg * kMaxD + c] = part;
+  pat_s[kg * D + c] = part;
   __syncthreads();
 
   if (threadIdx.x < D) {
     uint32_t pattern = 0;
-    for (int g = 0; g < nkg; ++g) pattern |= pat_s[g * kMaxD + threadIdx.x];
+#pragma unroll
+    for (int g = 0; g < NKG; ++g) pattern |= pat_s[g * D + threadIdx.x];
     const uint32_t bucket = inverse_gray16(pattern);
     key_s[threadIdx.x] = (bucket << 8) | (uint32_t)threadIdx.x;  // unique (bucket, column) key
     if (a.bucket_out) a.bucket_out[(size_t)it * D + threadIdx.x] = (uint16_t)bucket;
@@ -126,6 +135,7 @@ DA_DEV void hash_cta(const PrepArgs& a, int it, uint8_t* smem) {
   if (threadIdx.x < D) {
     const uint32_t mine = key_s[threadIdx.x];
     int rank = 0;
+#pragma unroll 16
     for (int j = 0; j < D; ++j) rank += key_s[j] < mine ? 1 : 0;
     perm_s[rank] = (uint8_t)threadIdx.x;
   }
@@ -136,22 +146,21 @@ DA_DEV void hash_cta(const PrepArgs& a, int it, uint8_t* smem) {
   }
   if (!a.qhat) return;
 
-  // Sampling: Q̂ rows of this block, 8 bf16 (16 B) per store.
+  // Sampling: Q̂ rows of this block, 8 bf16 (16 B) per store; lanes of a warp cover 4 rows.
   const int dg = D / a.G;
   const int half = (a.HB == 2) ? (qb & 1) : 0;
-  const int cpr = a.DR / 8;  // 16-byte chunks per Q̂ row
+  const int cpr_sh = ilog2(a.DR / 8);  // 16-byte chunks per Q̂ row = DR / 8
   uint16_t* qh = a.qhat + ((size_t)bh * a.N + r0) * a.DR;
-  for (int i = threadIdx.x; i < rows * cpr; i += kThreads) {
-    const int r = i / cpr, ch = i % cpr;
+  for (int i = threadIdx.x; i < (rows << cpr_sh); i += kThreads) {
+    const int r = i >> cpr_sh, ch = i & ((1 << cpr_sh) - 1);
     uint32_t w[4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       uint16_t v2[2];
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
-        const int col = ch * 8 + 2 * e + u;
-        const int j = col - half * dg;
-        v2[u] = (j >= 0 && j < dg) ? f2bf(load_f<T>(q_s + r * D + perm_s[j * a.G])) : (uint16_t)0;
+        const int j = ch * 8 + 2 * e + u - half * dg;
+        v2[u] = (j >= 0 && j < dg) ? f2bf(load_f<T>(q_s + r * QP + perm_s[j * a.G])) : (uint16_t)0;
       }
       w[e] = (uint32_t)v2[0] | ((uint32_t)v2[1] << 16);
     }
@@ -159,59 +168,78 @@ DA_DEV void hash_cta(const PrepArgs& a, int it, uint8_t* smem) {
   }
 }
 
-// K [N][d] -> K^T [d][N_pad] for one (bhkv, 64-key tile). The smem tile row pitch is d+2
-// elements (65 words for d=128) so that the transposed reads (8 key rows x 4 columns per warp)
-// hit 16 distinct banks; global reads are 16-byte vectors, global writes 128-byte row segments.
-template <typename T>
+// K [N][d] -> K^T [d][N_pad] for one (bhkv, 64-key tile).
+// Staging: tile[t][*] holds key t's d values in 16-byte chunks stored at chunk index
+// c8 ^ f(t), f(t) = (t & 7) ^ ((t >> 3 & 3) << 1): the 16-byte stores of a warp (2 keys x 16
+// chunks) and the 2-byte column reads of a warp (8 columns x 4 key octets, 8 keys each) both hit
+// distinct banks. Each thread then owns 8 consecutive keys of one column = one 16-byte chunk of
+// a K^T row; a warp writes 8 rows x 64 contiguous bytes.
+template <typename T, int D>
 DA_DEV void kt_cta(const PrepArgs& a, int it, uint8_t* smem) {
-  const int D = a.d;
-  const int ntile = (a.N + 63) / 64;
-  const int bhkv = it / ntile, t0 = (it % ntile) * 64;
+  constexpr int CPR = D / 8;  // 16-byte chunks per key row (bf16)
+  const int ntile = (a.N + 63) >> 6;
+  const int bhkv = it / ntile, t0 = (it - bhkv * ntile) * 64;
   const int nkeys = min(64, a.N - t0);
-  uint16_t* tile = reinterpret_cast<uint16_t*>(smem);  // [64][D + 2] bf16
-  const int ld = D + 2;
+  uint4* tile = reinterpret_cast<uint4*>(smem);  // [64][CPR] chunks
   const T* kg = reinterpret_cast<const T*>(a.k) + ((size_t)bhkv * a.N + t0) * D;
-  constexpr int VEC = 16 / sizeof(T);
-  const int vpr = D / VEC;  // 16-byte vectors per K row
-  for (int i = threadIdx.x; i < 64 * vpr; i += kThreads) {
-    const int t = i / vpr, cv = i % vpr;
-    uint32_t w[4] = {0u, 0u, 0u, 0u};
+  constexpr int NIT = 64 * CPR / kThreads;  // 4 (d=128) or 2 (d=64): all loads in flight first
+  uint4 w[NIT];
+#pragma unroll
+  for (int u = 0; u < NIT; ++u) {
+    const int i = threadIdx.x + u * kThreads;
+    const int t = i / CPR, c8 = i % CPR;
+    w[u] = make_uint4(0u, 0u, 0u, 0u);
     if (t < nkeys) {
-      const uint4 x = *reinterpret_cast<const uint4*>(kg + (size_t)t * D + cv * VEC);
       if (sizeof(T) == 2) {
-        w[0] = x.x; w[1] = x.y; w[2] = x.z; w[3] = x.w;
+        w[u] = *reinterpret_cast<const uint4*>(kg + (size_t)t * D + c8 * 8);
       } else {
-        w[0] = (uint32_t)f2bf(__uint_as_float(x.x)) | ((uint32_t)f2bf(__uint_as_float(x.y)) << 16);
-        w[1] = (uint32_t)f2bf(__uint_as_float(x.z)) | ((uint32_t)f2bf(__uint_as_float(x.w)) << 16);
+        const float4 x0 = *reinterpret_cast<const float4*>(kg + (size_t)t * D + c8 * 8);
+        const float4 x1 = *reinterpret_cast<const float4*>(kg + (size_t)t * D + c8 * 8 + 4);
+        w[u] = make_uint4((uint32_t)f2bf(x0.x) | ((uint32_t)f2bf(x0.y) << 16),
+                          (uint32_t)f2bf(x0.z) | ((uint32_t)f2bf(x0.w) << 16),
+                          (uint32_t)f2bf(x1.x) | ((uint32_t)f2bf(x1.y) << 16),
+                          (uint32_t)f2bf(x1.z) | ((uint32_t)f2bf(x1.w) << 16));
       }
     }
-    uint32_t* dst = reinterpret_cast<uint32_t*>(tile + t * ld + cv * VEC);
+  }
 #pragma unroll
-    for (int e = 0; e < VEC / 2; ++e) dst[e] = w[e];
+  for (int u = 0; u < NIT; ++u) {
+    const int i = threadIdx.x + u * kThreads;
+    const int t = i / CPR, c8 = i % CPR;
+    const int f = (t & 7) ^ (((t >> 3) & 3) << 1);
+    tile[t * CPR + (c8 ^ f)] = w[u];
   }
   __syncthreads();
-  // Each thread writes one 16-byte chunk: 8 consecutive keys of one K^T row (8 lanes = 128 B).
+  const uint16_t* te = reinterpret_cast<const uint16_t*>(tile);
   uint16_t* ktg = a.kt + (size_t)bhkv * D * a.N_pad;
+  // task -> (column c, key octet k8); lane = (k8 & 3) * 8 + (c & 7)
   for (int i = threadIdx.x; i < D * 8; i += kThreads) {
-    const int c = i / 8, ch = i % 8;
-    const int t = t0 + ch * 8;
-    if (t >= a.N_pad) continue;
+    const int lane = i & 31, grp = i >> 5;
+    const int c = (grp % (D / 8)) * 8 + (lane & 7);
+    const int k8 = (grp / (D / 8)) * 4 + (lane >> 3);
+    const int t = k8 * 8;
+    if (t0 + t >= a.N_pad) continue;
     uint32_t w[4];
 #pragma unroll
-    for (int e = 0; e < 4; ++e)
-      w[e] = (uint32_t)tile[(ch * 8 + 2 * e) * ld + c] | ((uint32_t)tile[(ch * 8 + 2 * e + 1) * ld + c] << 16);
-    *reinterpret_cast<uint4*>(ktg + (size_t)c * a.N_pad + t) = make_uint4(w[0], w[1], w[2], w[3]);
+    for (int e = 0; e < 4; ++e) {
+      const int ta = t + 2 * e, tb = ta + 1;
+      const int fa = (ta & 7) ^ (((ta >> 3) & 3) << 1), fb = (tb & 7) ^ (((tb >> 3) & 3) << 1);
+      const uint32_t lo = te[(ta * CPR + ((c >> 3) ^ fa)) * 8 + (c & 7)];
+      const uint32_t hi = te[(tb * CPR + ((c >> 3) ^ fb)) * 8 + (c & 7)];
+      w[e] = lo | (hi << 16);
+    }
+    *reinterpret_cast<uint4*>(ktg + (size_t)c * a.N_pad + t0 + t) = make_uint4(w[0], w[1], w[2], w[3]);
   }
 }
 
-template <typename T>
+template <typename T, int D>
 __global__ void __launch_bounds__(kThreads) prep_kernel(const PrepArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
   const int bid = blockIdx.x;
   if (bid < a.n_hash_ctas)
-    hash_cta<T>(a, bid, smem);
+    hash_cta<T, D>(a, bid, smem);
   else
-    kt_cta<T>(a, bid - a.n_hash_ctas, smem);
+    kt_cta<T, D>(a, bid - a.n_hash_ctas, smem);
 }
 
 __global__ void convert_kernel(const float* __restrict__ src, uint16_t* __restrict__ dst, size_t n) {
@@ -219,28 +247,30 @@ __global__ void convert_kernel(const float* __restrict__ src, uint16_t* __restri
     dst[i] = f2bf(src[i]);
 }
 
-}  // namespace
-
-size_t prep_smem_bytes(int in_f32) {
-  const size_t q = (size_t)kMaxL * kMaxD * (in_f32 ? 4 : 2);
-  return q + kMaxL * 16 * 4 + 4 * kMaxD * 4 + kMaxD * 4 + kMaxD + 16;
+template <typename T, int D>
+size_t prep_smem_bytes() {
+  const size_t q = (size_t)kMaxL * q_pitch<T, D>() * sizeof(T);
+  const size_t hash = q + kMaxL * 16 * 4 + 4 * D * 4 + D * 4 + D + 16;
+  const size_t kt = 64 * D * 2;
+  return std::max(hash, kt);
 }
 
-cudaError_t launch_prep(const PrepArgs& a, cudaStream_t st) {
+template <typename T, int D>
+cudaError_t launch_prep_t(const PrepArgs& a, cudaStream_t st) {
   const int grid = a.n_hash_ctas + a.n_kt_ctas;
-  if (grid == 0) return cudaSuccess;
-  const size_t smem = prep_smem_bytes(a.in_f32);
-  cudaError_t e;
-  if (a.in_f32) {
-    e = cudaFuncSetAttribute(prep_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    prep_kernel<float><<<grid, kThreads, smem, st>>>(a);
-  } else {
-    e = cudaFuncSetAttribute(prep_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    prep_kernel<uint16_t><<<grid, kThreads, smem, st>>>(a);
-  }
+  const size_t smem = prep_smem_bytes<T, D>();
+  cudaError_t e = cudaFuncSetAttribute(prep_kernel<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  prep_kernel<T, D><<<grid, kThreads, smem, st>>>(a);
   return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_prep(const PrepArgs& a, cudaStream_t st) {
+  if (a.n_hash_ctas + a.n_kt_ctas == 0) return cudaSuccess;
+  if (a.in_f32) return a.d == 64 ? launch_prep_t<float, 64>(a, st) : launch_prep_t<float, 128>(a, st);
+  return a.d == 64 ? launch_prep_t<uint16_t, 64>(a, st) : launch_prep_t<uint16_t, 128>(a, st);
 }
 
 cudaError_t launch_convert_bf16(const float* src, uint16_t* dst, size_t n, cudaStream_t st) {
