@@ -1,0 +1,69 @@
+"""Per-config timings (distr vs own exact kernel) for every BASELINE.json config + the C4 N sweep.
+
+    python tools/sweep.py [--steps K] > gpurun_out/sweep.json   (one JSON line per case)
+
+Kernel times come from CUDA events recorded around the launches inside the C call
+(distr_attn_set_profile_events); inputs are regenerated per case on the device.
+"""
+import argparse, ctypes, json, os, sys
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch
+import paper_2507_17245_b200 as da
+from paper_2507_17245_b200 import _native
+from synth import CONFIGS, C4_SWEEP_N, make_qkv
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--steps", type=int, default=10)
+ap.add_argument("--warmup", type=int, default=3)
+args = ap.parse_args()
+L = _native.lib()
+cases = [("C1", CONFIGS["C1"]), ("C2", CONFIGS["C2"]), ("C3", CONFIGS["C3"])]
+cases += [(f"C4 N={n} G*={g}", CONFIGS["C4"].with_(N=n, group_size=g)) for n in C4_SWEEP_N for g in (2, 4)]
+cases += [("C5 1-GPU", CONFIGS["C5"])]
+
+
+def timed(fn):
+    for _ in range(args.warmup):
+        fn(None)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    for e3 in evs:
+        for e in e3:
+            e.record()
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for e3 in evs:
+        fn(e3)
+    t1.record()
+    torch.cuda.synchronize()
+    attn = sum(e[1].elapsed_time(e[2]) for e in evs) / args.steps
+    return t0.elapsed_time(t1) / args.steps, attn
+
+
+for name, c in cases:
+    q, k, v = make_qkv(c, device="cuda")
+    out = torch.empty_like(q)
+
+    def run(evs, exact=False):
+        if evs is not None:
+            L.distr_attn_set_profile_events(*[ctypes.c_void_p(e.cuda_event) for e in evs])
+        if exact:
+            da.exact_attn_fwd_ex(q, k, v, out, block_l=c.block_l, causal=c.causal)
+        else:
+            da.distr_attn_fwd_ex(q, k, v, out, block_l=c.block_l, group_size=c.group_size, causal=c.causal)
+
+    d_ms, d_attn = timed(lambda e: run(e))
+    x_ms, x_attn = timed(lambda e: run(e, True))
+    pairs = c.B * c.H * c.N * c.N * (0.5 if c.causal else 1.0)
+    DR = (128 // c.block_l) * c.d // c.group_size
+    rec = {"case": name, "B": c.B, "H": c.H, "H_kv": c.H_kv, "N": c.N, "d": c.d, "block_l": c.block_l,
+           "G": c.group_size, "causal": c.causal, "dtype": c.dtype,
+           "distr_ms": d_ms, "distr_attn_kernel_ms": d_attn, "exact_ms": x_ms, "exact_attn_kernel_ms": x_attn,
+           "speedup": x_ms / d_ms,
+           "distr_tflops_executed": pairs * (2 * DR + 2 * c.d) / (d_attn * 1e-3) / 1e12,
+           "exact_tflops": pairs * 4 * c.d / (x_attn * 1e-3) / 1e12,
+           "full_d_equiv_tflops": pairs * 4 * c.d / (d_ms * 1e-3) / 1e12}
+    print(json.dumps(rec), flush=True)
+    del q, k, v, out
+    torch.cuda.empty_cache()
