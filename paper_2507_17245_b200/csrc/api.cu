@@ -163,9 +163,11 @@ int validate(const da_params* p, bool distr, Plan* P) {
   size_t o = 0;
   q.off_perm = q.off_qhat = q.off_kt = q.off_qc = q.off_kc = q.off_vc = 0;
   if (distr) {
-    q.off_perm = o; o = al256(o + BH * q.nqb * q.d);
-    q.off_qhat = o; o = al256(o + BH * q.N * q.DR * 2);
-    q.off_kt = o;   o = al256(o + BHkv * q.d * q.N_pad * 2);
+    // bf16: the attention CTA hashes its own Q blocks, only K^T is precomputed.
+    // fp32: the prep kernel hashes the fp32 values (bit-exact contract) -> perm; Q, V -> bf16.
+    if (q.f32) { q.off_perm = o; o = al256(o + BH * q.nqb * q.d); }
+    q.off_kt = o; o = al256(o + BHkv * q.d * q.N_pad * 2);
+    if (q.f32) { q.off_qc = o; o = al256(o + BH * q.N * q.d * 2); }
   } else if (q.f32) {
     q.off_qc = o; o = al256(o + BH * q.N * q.d * 2);
     q.off_kc = o; o = al256(o + BHkv * q.N * q.d * 2);
@@ -277,16 +279,24 @@ int forward(const void* q, const void* k, const void* v, void* out, const da_par
     a.q = q; a.k = k; a.in_f32 = P.f32;
     a.BH = (int)BH; a.BHkv = (int)BHkv; a.N = P.N; a.d = P.d; a.block_l = P.l; a.G = P.G; a.HB = P.HB;
     a.DR = P.DR; a.nqb = P.nqb; a.N_pad = P.N_pad; a.proj = proj;
-    a.perm_ws = ws + P.off_perm;
-    a.bucket_out = p->bucket_ids;
-    a.perm_out = p->perm;
-    a.qhat = reinterpret_cast<uint16_t*>(ws + P.off_qhat);
     a.kt = reinterpret_cast<uint16_t*>(ws + P.off_kt);
-    a.n_hash_ctas = (int)(BH * P.nqb);
     a.n_kt_ctas = (int)(BHkv * ((P.N + 63) / 64));
+    if (P.f32) {  // hash the fp32 values in the prep kernel; the attention kernel reads perm
+      a.perm_ws = ws + P.off_perm;
+      a.bucket_out = p->bucket_ids;
+      a.perm_out = p->perm;
+      a.n_hash_ctas = (int)(BH * P.nqb);
+    }
     DA_CUDA(da::launch_prep(a, st));
     ++launches;
-    a_src = a.qhat;
+    if (P.f32) {
+      uint16_t* qc = reinterpret_cast<uint16_t*>(ws + P.off_qc);
+      DA_CUDA(da::launch_convert_bf16(static_cast<const float*>(q), qc, BH * P.N * P.d, st));
+      ++launches;
+      a_src = qc;
+    } else {
+      a_src = q;
+    }
     k_src = a.kt;
   } else if (P.f32) {
     uint16_t* qc = reinterpret_cast<uint16_t*>(ws + P.off_qc);
@@ -302,12 +312,10 @@ int forward(const void* q, const void* k, const void* v, void* out, const da_par
   }
 
   CUtensorMap tmA, tmK, tmV;
+  if (int s = make_map(&tmA, a_src, P.d, P.N, BH, 64, 128, 128)) return s;  // natural Q tiles
   if (distr) {
-    const int sw = P.DR * 2 >= 128 ? 128 : P.DR * 2;
-    if (int s = make_map(&tmA, a_src, P.DR, P.N, BH, sw / 2, 128, sw)) return s;
     if (int s = make_map(&tmK, k_src, P.N_pad, P.d, BHkv, 128, P.d, 0)) return s;
   } else {
-    if (int s = make_map(&tmA, a_src, P.d, P.N, BH, 64, 128, 128)) return s;
     if (int s = make_map(&tmK, k_src, P.d, P.N, BHkv, 64, 128, 128)) return s;
   }
   if (int s = make_map(&tmV, kv_v, P.d, P.N, BHkv, 64, 128, 128)) return s;
@@ -316,7 +324,10 @@ int forward(const void* q, const void* k, const void* v, void* out, const da_par
   aa.N = P.N; aa.H = P.H; aa.H_kv = P.Hkv; aa.nqt = P.nqt; aa.nkt = P.nkt; aa.nqb = P.nqb; aa.block_l = P.l;
   aa.scale_log2 = P.scale * 1.4426950408889634f;
   aa.causal = P.causal;
-  aa.perm = distr ? ws + P.off_perm : nullptr;
+  aa.perm = (distr && P.f32) ? ws + P.off_perm : nullptr;
+  aa.proj = distr ? proj : nullptr;
+  aa.bucket_out = (distr && !P.f32) ? p->bucket_ids : nullptr;
+  aa.perm_out = (distr && !P.f32) ? p->perm : nullptr;
   aa.out = out;
   aa.out_f32 = P.f32;
   aa.lse = p->lse;

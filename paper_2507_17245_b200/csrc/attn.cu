@@ -66,6 +66,11 @@ struct Cfg {
   static constexpr int OFF_BAR = OFF_PERM + 2 * 2 * 128;
   static constexpr int SMEM = OFF_BAR + 256 + 6144 + 1024;  // barriers, row-max/sum exchange, align slack
   static constexpr uint32_t A_LAYOUT = A_SW == 128 ? kSw128 : (A_SW == 64 ? kSw64 : kSw32);
+  static constexpr int A_SWB = A_SW == 128 ? 3 : (A_SW == 64 ? 2 : 1);  // Swizzle<B,4,3> bits
+  // distr: the natural Q tiles (K-major SW128 boxes, 128 rows x d) are staged for the in-CTA
+  // hash / Q̂ build in the V ring, or in the K+V rings when the V ring alone is too small.
+  static constexpr int QT_BYTES = BM * D * 2;
+  static constexpr bool STAGE_IN_V = NS * V_BYTES >= 2 * QT_BYTES;
   static_assert(DR % 16 == 0 && DR >= 16 && DR <= 128, "reduced width");
   static_assert(A_COLS % A_BOX_COLS == 0, "A boxes");
   static_assert(SMEM <= 232448, "shared memory");
@@ -83,9 +88,168 @@ enum {
   B_SFULL = 17,   // +t
   B_PFULL = 19,   // +t
   B_OFULL = 21,   // +t
-  B_TMEMPTR = 23,
-  B_COUNT = 24
+  B_QHAT = 23,    // distr: Q̂ of both tiles built in sA (384 hashing threads arrive)
+  B_TMEMPTR = 24,
+  B_COUNT = 25
 };
+
+// Swizzle<B,4,3>: XOR byte-address bits [4, 4+B) with bits [7, 7+B) — the TMA / UMMA
+// SWIZZLE_{32,64,128}B layouts (B = 1, 2, 3), valid inside 1024-byte aligned regions.
+DA_DEV uint32_t swz(uint32_t a, int B) { return a ^ (((a >> 7) & ((1u << B) - 1u)) << 4); }
+
+DA_DEV uint32_t inverse_gray16(uint32_t p) {
+  p ^= p >> 1;
+  p ^= p >> 2;
+  p ^= p >> 4;
+  p ^= p >> 8;
+  return p & 0xFFFFu;
+}
+
+// LSH + grouping + sampling of the CTA's two Q tiles (§3.2-3.3), run by the 384
+// worker threads (warps 4-15) before their roles start. Same arithmetic as prep.cu hash_cta
+// (bit-exact contract with the oracle: fp32 fma chain in ascending rows from +0, strict y > 0,
+// LSB = projection row 0, inverse Gray, stable rank by (bucket, column)):
+//   staged Q (natural, SW128 K-major boxes) -> y[16] per (tile, hash block, column) -> perm_s
+//   -> Q̂ rows gathered into sA in the A operand's swizzled K-major layout.
+// With args.perm set (fp32 inputs) the permutations come from the prep kernel instead.
+template <class C, int D, int G, int HB>
+DA_DEV void qhat_prologue(const AttnArgs& args, uint64_t* bars, const uint8_t* sQ, uint8_t* sA, uint8_t* scratch,
+                          uint8_t* perm_s, int bh, int qt0, int ntile, int ht, long long* trace) {
+#define PT(i) if (trace && ht == 0) trace[15 * 256 + (i)] = clock64();
+  PT(0)
+  constexpr int NW = 384;
+  constexpr int DG = D / G;
+  const int L = args.block_l;
+  float* proj_t = reinterpret_cast<float*>(scratch);           // [l][16]
+  uint32_t* key_s = reinterpret_cast<uint32_t*>(scratch + 8192);  // [2][HB][D] keys + [2][HB][D][2] u8 parts
+  auto wsync = [] { asm volatile("bar.sync 5, 384;" ::: "memory"); };
+  auto q_at = [&](int t, int r, int c) -> uint32_t {  // bf16 bits of staged Q(t, r, c)
+    const uint32_t off = (uint32_t)(t * C::QT_BYTES + (c >> 6) * (BM * 128) + r * 128 + (c & 63) * 2);
+    return *reinterpret_cast<const uint16_t*>(sQ + swz(off, 3));
+  };
+  const bool hash = args.perm == nullptr;
+  if (hash)
+    for (int i = ht; i < 16 * L; i += NW) proj_t[(i % L) * 16 + i / L] = args.proj[i];
+  mbar_wait(&bars[B_Q], 0);
+  wsync();
+  PT(1)
+  if (hash) {
+    // Projection: unit = (tile, hash block, column pair, half of the 16 projection rows): per row
+    // one 4-byte load of the two columns, two 16-byte (broadcast) projection loads, 8 FFMA2.
+    // The halves' 8-bit patterns are OR-ed through shared memory.
+    const int nunits = ntile * HB * D;
+    for (int u2 = ht; u2 < nunits; u2 += NW) {  // u2 = ((tile, hb, column pair) << 1) | k-half
+      const int kh = u2 & 1, cp = u2 >> 1;       // cp indexes (t, hb, c/2)
+      const int t = cp / (HB * D / 2), hb = (cp / (D / 2)) % HB, c = (cp % (D / 2)) * 2;
+      const int row0 = (qt0 + t) * BM + hb * L;  // first global row of this hash block
+      const int rows = max(0, min(L, args.N - row0));
+      // staged Q(t, hb*L + r, c): box c/64, row stride 128 B, 16-B chunk ((c%64)/8) ^ (row%8)
+      const uint8_t* qcol = sQ + t * C::QT_BYTES + (c >> 6) * (BM * 128) + hb * L * 128 + (c & 7) * 2;
+      const uint32_t chunk = (uint32_t)((c & 63) >> 3);
+      float2 ya[4], yb[4];  // column c / c+1, projection rows 8kh .. 8kh+7
+#pragma unroll
+      for (int m = 0; m < 4; ++m) ya[m] = yb[m] = make_float2(0.0f, 0.0f);
+      const float* pr = proj_t + 8 * kh;
+#pragma unroll 2
+      for (int r = 0; r < rows; ++r) {
+        const uint32_t q2 = *reinterpret_cast<const uint32_t*>(qcol + r * 128 + ((chunk ^ (uint32_t)(r & 7)) << 4));
+        const float qa = __uint_as_float(q2 << 16), qb = __uint_as_float(q2 & 0xFFFF0000u);
+        const float4 p0 = *reinterpret_cast<const float4*>(pr + r * 16);
+        const float4 p1 = *reinterpret_cast<const float4*>(pr + r * 16 + 4);
+        const float2 pk[4] = {make_float2(p0.x, p0.y), make_float2(p0.z, p0.w), make_float2(p1.x, p1.y),
+                              make_float2(p1.z, p1.w)};
+#pragma unroll
+        for (int m = 0; m < 4; ++m) {
+          ya[m] = fma2(pk[m], make_float2(qa, qa), ya[m]);
+          yb[m] = fma2(pk[m], make_float2(qb, qb), yb[m]);
+        }
+      }
+      uint32_t ba = 0, bb = 0;
+#pragma unroll
+      for (int m = 0; m < 4; ++m) {
+        ba |= (ya[m].x > 0.0f ? 1u : 0u) << (2 * m) | (ya[m].y > 0.0f ? 1u : 0u) << (2 * m + 1);
+        bb |= (yb[m].x > 0.0f ? 1u : 0u) << (2 * m) | (yb[m].y > 0.0f ? 1u : 0u) << (2 * m + 1);
+      }
+      uint8_t* parts = reinterpret_cast<uint8_t*>(key_s + 2 * HB * D);  // [unit][2 halves]
+      const int u = (t * HB + hb) * D + c;
+      parts[2 * u + kh] = (uint8_t)ba;
+      parts[2 * (u + 1) + kh] = (uint8_t)bb;
+    }
+    wsync();
+    for (int u = ht; u < nunits; u += NW) {
+      const uint32_t pattern = reinterpret_cast<const uint16_t*>(key_s + 2 * HB * D)[u];  // halves lo | hi << 8
+      const uint32_t bucket = inverse_gray16(pattern);
+      const int t = u / (HB * D), hb = (u / D) % HB, c = u % D;
+      key_s[u] = (bucket << 8) | (uint32_t)c;
+      const int row0 = (qt0 + t) * BM + hb * L;
+      if (args.bucket_out && row0 < args.N)
+        args.bucket_out[((size_t)bh * args.nqb + row0 / L) * D + c] = (uint16_t)bucket;
+    }
+    wsync();
+    PT(2)
+    for (int u = ht; u < nunits; u += NW) {
+      const uint4* ks = reinterpret_cast<const uint4*>(key_s + (u / D) * D);
+      const uint32_t mine = key_s[u];
+      int rank = 0;
+#pragma unroll 8
+      for (int j = 0; j < D / 4; ++j) {
+        const uint4 k4 = ks[j];
+        rank += (k4.x < mine ? 1 : 0) + (k4.y < mine ? 1 : 0) + (k4.z < mine ? 1 : 0) + (k4.w < mine ? 1 : 0);
+      }
+      const int c = u % D;
+      perm_s[(u / D) * D + rank] = (uint8_t)c;
+      const int qb = ((qt0 + u / (HB * D)) * BM) / L + (u / D) % HB;
+      if (args.perm_out && qb < args.nqb)
+        args.perm_out[((size_t)bh * args.nqb + qb) * D + rank] = (uint8_t)c;
+    }
+  } else {
+    for (int u = ht; u < ntile * HB * D; u += NW) {
+      const int t = u / (HB * D), hb = (u / D) % HB, c = u % D;
+      const int qb = (qt0 + t) * BM / L + hb;
+      perm_s[u] = (qb < args.nqb) ? args.perm[((size_t)bh * args.nqb + qb) * D + c] : (uint8_t)c;
+    }
+  }
+  wsync();
+  PT(3)
+  // Q̂[r][j] = Q[r][perm[j G]] (sampling); block_l = 64 stacks the two hash blocks of a tile
+  // block-diagonally (columns [hb*d/G*, (hb+1)*d/G*) of rows of hash block hb, zeros elsewhere).
+  constexpr int CPR = C::DR / 8;
+  constexpr int NCOMBO = 2 * CPR;          // (tile, chunk) pairs
+  constexpr int TPC = NW / NCOMBO;         // threads per pair (rows strided by TPC)
+  const int combo = ht % NCOMBO, rstart = ht / NCOMBO;
+  const int t = combo / CPR, ch = combo % CPR;
+  if (t < ntile && rstart < TPC) {
+    // the 8 source columns of this 16-byte chunk (or -1 = zero) for each row-parity class
+    int src[2][8];
+#pragma unroll
+    for (int hbr = 0; hbr < 2; ++hbr)
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int j = ch * 8 + e, hbj = j / DG, jj = j % DG;
+        src[hbr][e] = (HB == 2 && hbj != hbr) || (HB == 1 && hbr == 1) ? -1 : perm_s[(t * HB + hbj) * D + jj * G];
+      }
+    const int j0 = ch * 8;
+    const uint32_t dcol = (uint32_t)((j0 / C::A_BOX_COLS) * C::A_BOX_BYTES + (j0 % C::A_BOX_COLS) * 2);
+    for (int r = rstart; r < BM; r += TPC) {
+      const int hbr = HB == 2 ? r / 64 : 0;
+      uint32_t v[8];
+#pragma unroll
+      for (int e = 0; e < 8; ++e) {
+        const int c = src[hbr][e];
+        v[e] = c < 0 ? 0u
+                     : *reinterpret_cast<const uint16_t*>(
+                           sQ + t * C::QT_BYTES + (c >> 6) * (BM * 128) + r * 128 +
+                           ((((uint32_t)(c & 63) >> 3) ^ (uint32_t)(r & 7)) << 4) + (c & 7) * 2);
+      }
+      *reinterpret_cast<uint4*>(sA + t * C::A_BYTES + swz(dcol + r * C::A_SW, C::A_SWB)) =
+          make_uint4(v[0] | (v[1] << 16), v[2] | (v[3] << 16), v[4] | (v[5] << 16), v[6] | (v[7] << 16));
+    }
+  }
+  fence_proxy_async_smem();
+  mbar_arrive(&bars[B_QHAT]);
+  PT(4)
+#undef PT
+}
 
 // EMU: number of every 8 column pairs whose exp2 runs as a polynomial on the FMA pipe instead of
 // MUFU.EX2 (16 ex2/clk/SM, one per (query, key) pair — it co-bounds the tile with the tensor
@@ -127,6 +291,7 @@ __global__ void __launch_bounds__(threads_of<DISTR>(), 1)
 
   if (threadIdx.x == 0) {
     mbar_init(&bars[B_Q], 1);
+    mbar_init(&bars[B_QHAT], 384);
     for (int s = 0; s < NS; ++s) {
       mbar_init(&bars[B_KFULL + s], 1);
       mbar_init(&bars[B_KEMPTY + s], DISTR ? kFusionThreads : 1);
@@ -143,25 +308,40 @@ __global__ void __launch_bounds__(threads_of<DISTR>(), 1)
       mbar_init(&bars[B_OFULL + t], 1);
     }
     fence_mbar_init();
+    // A operand, issued before anything else: exact -> Q tiles straight into sA; distr -> natural
+    // Q tiles into the staging area, from which the 384 worker threads hash the Q blocks and
+    // build Q̂ in sA (qhat_prologue).
+    tma_prefetch_desc(&tmA);
+    tma_prefetch_desc(&tmK);
+    tma_prefetch_desc(&tmV);
+    const int ntile = nkt_t[1] > 0 ? 2 : 1;
+    if (DISTR) {
+      uint8_t* sQ0 = C::STAGE_IN_V ? sV : sK;
+      mbar_arrive_expect_tx(&bars[B_Q], ntile * C::QT_BYTES);
+      for (int t = 0; t < ntile; ++t)
+        for (int bx = 0; bx < D / 64; ++bx)
+          tma_load_3d(sQ0 + t * C::QT_BYTES + bx * (BM * 128), &tmA, &bars[B_Q], bx * 64, (qt0 + t) * BM, bh);
+    } else {
+      mbar_arrive_expect_tx(&bars[B_Q], ntile * C::A_BYTES);
+      for (int t = 0; t < ntile; ++t)
+        for (int bx = 0; bx < C::A_NBOX; ++bx)
+          tma_load_3d(sA + t * C::A_BYTES + bx * C::A_BOX_BYTES, &tmA, &bars[B_Q], bx * C::A_BOX_COLS,
+                      (qt0 + t) * BM, bh);
+    }
   }
   if (warp == 1) {
     tmem_alloc(tmem_ptr_s, kTmemCols);
     tmem_relinquish();
   }
-  if (DISTR && warp >= 12) {
-    // Permutation(s) of both tiles: hash block(s) covering rows [128*qt, 128*qt + 128).
-    const int ft = threadIdx.x - 384;
-    for (int i = ft; i < 2 * HB * D; i += kFusionThreads) {
-      const int t = i / (HB * D), hb = (i / D) % HB, c = i % D;
-      const int qb = (qt0 + t) * BM / args.block_l + hb;
-      perm_s[(t * HB + hb) * D + c] =
-          (qb < args.nqb) ? args.perm[((size_t)bh * args.nqb + qb) * D + c] : (uint8_t)c;
-    }
-  }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_ptr_s;
+
+  uint8_t* sQst = C::STAGE_IN_V ? sV : sK;
+  if (DISTR && warp >= 4)
+    qhat_prologue<C, D, G, HB>(args, bars, sQst, sA, sKh, perm_s, bh, qt0, nkt_t[1] > 0 ? 2 : 1,
+                               (int)threadIdx.x - 128, trace);
 
   // Register split (distr, 512 threads at 128 registers): the TMA/MMA warpgroup gives 64 of its
   // registers to the softmax warpgroups (128*64 + 256*160 + 128*128 = 512*128; an .inc that
@@ -176,15 +356,8 @@ __global__ void __launch_bounds__(threads_of<DISTR>(), 1)
   if (warp == 0) {
     // ------------------------------------------------------------------ TMA producer
     if (lane == 0) {
-      tma_prefetch_desc(&tmA);
-      tma_prefetch_desc(&tmK);
-      tma_prefetch_desc(&tmV);
-      const int ntile = nkt_t[1] > 0 ? 2 : 1;
-      mbar_arrive_expect_tx(&bars[B_Q], ntile * C::A_BYTES);
-      for (int t = 0; t < ntile; ++t)
-        for (int bx = 0; bx < C::A_NBOX; ++bx)
-          tma_load_3d(sA + t * C::A_BYTES + bx * C::A_BOX_BYTES, &tmA, &bars[B_Q], bx * C::A_BOX_COLS,
-                      (qt0 + t) * BM, bh);
+      // the staging area overlaps the K ring: wait until Q̂ is built
+      if (DISTR && !C::STAGE_IN_V) mbar_wait(&bars[B_QHAT], 0);
       // K (or K^T) ring; V has its own producer (warp 2) so K prefetch never waits behind the
       // PV that frees a V stage.
       for (int i = 0; i < nk; ++i) {
@@ -203,6 +376,7 @@ __global__ void __launch_bounds__(threads_of<DISTR>(), 1)
   } else if (warp == 2) {
     // ------------------------------------------------------------------ TMA producer (V ring)
     if (lane == 0) {
+      if (DISTR) mbar_wait(&bars[B_QHAT], 0);  // the V ring doubles as the Q staging area
       for (int i = 0; i < nk; ++i) {
         const int s = i % NS;
         const uint32_t ph = (i / NS) & 1;
@@ -268,7 +442,7 @@ __global__ void __launch_bounds__(threads_of<DISTR>(), 1)
       };
       auto release_v = [&](int j) { mma_commit(&bars[B_VEMPTY + j % NS]); };
 
-      mbar_wait(&bars[B_Q], 0);
+      mbar_wait(&bars[DISTR ? B_QHAT : B_Q], 0);
       tc_fence_after();
       for (int i = 0; i < nk; ++i) {
         // tile 0: PV_0(i-1) then S_0(i)   (S_0(i) overwrites P_0(i-1): in-order after the PV)

@@ -29,7 +29,11 @@ struct AttnArgs {
   int N, H, H_kv, nqt, nkt, nqb, block_l;
   float scale_log2;  // scale * log2(e)
   int causal;
-  const uint8_t* perm;  // [BH][nqb][d] (distr only)
+  const uint8_t* perm;  // [BH][nqb][d] precomputed permutations (distr, fp32 inputs) or NULL:
+                        // NULL = the attention CTA hashes its own Q blocks (bf16 inputs)
+  const float* proj;    // [16][block_l] projection matrix (distr, in-kernel hashing)
+  uint16_t* bucket_out; // optional exports [BH][nqb][d] (in-kernel hashing)
+  uint8_t* perm_out;
   void* out;            // [BH][N][d]
   int out_f32;
   float* lse;           // optional [BH][N]

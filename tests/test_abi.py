@@ -91,11 +91,14 @@ def test_null_pointers_rejected(L):
 
 
 def test_workspace_size_formula(L):
-    # distr: perm [BH][nqb][d] + Q̂ [BH][N][DR] bf16 + K^T [BHkv][d][N_pad] bf16 (256-B aligned)
+    # distr, bf16: only K^T [BHkv][d][N_pad] bf16 (the attention CTA hashes its own Q blocks)
     p = params(B=2, H=4, N=1000, d=128, block_l=128, G=2)
-    BH, nqb, N_pad, DR = 8, 8, 1000, 64
+    BH, nqb, N_pad = 8, 8, 1000
     al = lambda x: (x + 255) // 256 * 256
-    want = al(BH * nqb * 128) + al(BH * 1000 * DR * 2) + al(BH * 128 * N_pad * 2)
+    assert L.distr_attn_workspace_size(ctypes.byref(p)) == al(BH * 128 * N_pad * 2)
+    # distr, fp32: perm [BH][nqb][d] + K^T + bf16 copies of Q and V
+    p = params(B=2, H=4, N=1000, d=128, block_l=128, G=2, dtype=1)
+    want = al(BH * nqb * 128) + al(BH * 128 * N_pad * 2) + 2 * al(BH * 1000 * 128 * 2)
     assert L.distr_attn_workspace_size(ctypes.byref(p)) == want
 
 

@@ -20,6 +20,10 @@ t0 = t[t > 0].min()
 names = {0: "sm0 S ready", 1: "sm0 max done", 2: "sm0 P arrive", 3: "sm1 S ready", 4: "sm1 max done", 5: "sm1 P arrive",
          6: "mma S0 issued", 7: "mma S1 issued", 8: "mma P0 seen", 9: "mma P1 seen", 10: "fus K ready", 11: "fus K0 done", 12: "fus K1 done",
          13: "sm0 wait start", 14: "sm1 wait start"}
+pro = t[15, :5]
+if pro[0] > 0:
+    print("prologue (cycles from start): proj loaded+Q landed", pro[1]-pro[0], " hash", pro[2]-pro[1], " rank", pro[3]-pro[2], " qhat", pro[4]-pro[3], " total", pro[4]-pro[0])
+    print("first S0 ready after prologue end:", t[0, 0] - pro[4])
 for i in list(range(0, 6)) + list(range(60, 64)):
     print(f"--- tile {i}")
     ev = sorted([(t[s, i] - t0, n) for s, n in names.items() if t[s, i] > 0])
