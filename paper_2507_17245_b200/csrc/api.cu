@@ -225,17 +225,19 @@ int current_device(int* dev) {
 }
 
 // Share of exp2 pairs (out of 8) evaluated by polynomial on the FMA pipe instead of MUFU.EX2.
-// Measured on B200 (profiles/r01_v2): with the ping-pong softmax the MUFU is not the binding
-// unit (XU pipe < 50 % busy) and every emulated pair costs issue slots the softmax warpgroups
-// need, so the default is 0 for every flavour. DA_EMU overrides (0, 2, 3, 4) for tuning.
+// Measured on B200 (profiles/r01_v4): the exp phase of a tile is MUFU-bound
+// (16 ex2/clk/SM); moving 2/8 of the pairs to the FMA pipe shortens it by ~10 % and helps the
+// distr kernel, whose tensor-core block is shorter than the softmax; the exact kernel is then
+// co-bound by its longer tensor block and loses (power draw), so it keeps 0. DA_EMU overrides
+// (0, 2, 3, 4) for tuning.
 int default_emu(const Plan& P, bool distr) {
   static int env = [] {
     const char* e = getenv("DA_EMU");
     return e ? atoi(e) : -1;
   }();
   (void)P;
-  (void)distr;
-  return env >= 0 ? env : 0;
+  if (env >= 0) return env;
+  return distr ? 2 : 0;
 }
 
 // ---------------------------------------------------------------------------- forward
