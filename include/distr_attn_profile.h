@@ -16,7 +16,7 @@ extern "C" {
 int distr_attn_set_profile_events(void* ev_start, void* ev_attn, void* ev_end);
 
 /* One-shot debug timeline: the next forward call on this thread makes CTA (0,0) of the attention
- * kernel write clock64() stamps of its pipeline events into device_buf (int64 [16][256], caller
+ * kernel write clock64() stamps of its pipeline events into device_buf (int64 [20][256], caller
  * owned; slot meanings in attn.cu). NULL disarms. Returns DA_OK. */
 int distr_attn_set_trace(void* device_buf);
 #ifdef __cplusplus

@@ -561,9 +561,11 @@ __global__ void __launch_bounds__(threads_of<DISTR>(), 1)
             p = make_float2(ex2(x.x), ex2(x.y));
           acc[e & 3] = fadd2(acc[e & 3], p);
           pr[e] = pack_bf16x2(p.x, p.y);
+          // P of keys [64*half, 64*half + 64) -> columns [32*half, 32*half + 32) of S_t, stored
+          // in 8-column chunks as they complete so the TMEM writes drain under the remaining exps
+          if ((e & 7) == 7) tmem_st8(tmem + lane_base + kColS + 128u * t + 32u * half + (e - 7), &pr[e - 7]);
         }
-        // P of keys [64*half, 64*half + 64) -> columns [32*half, 32*half + 32) of S_t
-        tmem_st32(tmem + lane_base + kColS + 128u * t + 32u * half, pr);
+        DA_TRACE(16 + t, i, row == 0 && half == 0);
         const float2 a = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
         l[t] += a.x + a.y;
         tmem_st_wait();

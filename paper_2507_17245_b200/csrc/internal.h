@@ -37,7 +37,7 @@ struct AttnArgs {
   void* out;            // [BH][N][d]
   int out_f32;
   float* lse;           // optional [BH][N]
-  long long* trace;     // optional debug timeline of CTA (0,0): clock64() stamps, [16][256]
+  long long* trace;     // optional debug timeline of CTA (0,0): clock64() stamps, [20][256]
 };
 
 cudaError_t launch_prep(const PrepArgs& a, cudaStream_t st);

@@ -11,11 +11,11 @@ c = Config("t", 1, 16, 16, N, 128, 128, 2, False, "bf16", 5)
 q, k, v = make_qkv(c, device="cuda")
 f = (lambda: da.distr_attn_fwd_ex(q, k, v, block_l=128, group_size=2)) if mode == "distr" else (lambda: da.exact_attn_fwd_ex(q, k, v, block_l=128))
 for _ in range(3): f()
-buf = torch.zeros(16 * 256, dtype=torch.int64, device="cuda")
+buf = torch.zeros(20 * 256, dtype=torch.int64, device="cuda")
 torch.cuda.synchronize()
 _native.lib().distr_attn_set_trace(ctypes.c_void_p(buf.data_ptr()))
 f(); torch.cuda.synchronize()
-t = buf.cpu().numpy().reshape(16, 256).astype(np.int64)
+t = buf.cpu().numpy().reshape(20, 256).astype(np.int64)
 t0 = t[t > 0].min()
 names = {0: "sm0 S ready", 1: "sm0 max done", 2: "sm0 P arrive", 3: "sm1 S ready", 4: "sm1 max done", 5: "sm1 P arrive",
          6: "mma S0 issued", 7: "mma S1 issued", 8: "mma P0 seen", 9: "mma P1 seen", 10: "fus K ready", 11: "fus K0 done", 12: "fus K1 done",
@@ -33,6 +33,7 @@ def d(a, b, lo=20, hi=100): return np.median(t[b, lo:hi] - t[a, lo:hi])
 print("median cycles (tiles 20..100):")
 print("  sm0: wait S   ", d(13, 0), " S->max", d(0, 1), " max->P", d(1, 2), " period", np.median(np.diff(t[2, 20:100])))
 print("  sm1: wait S   ", d(14, 3), " S->max", d(3, 4), " max->P", d(4, 5), " period", np.median(np.diff(t[5, 20:100])))
+print("  sm0 max->expdone", d(1, 16), " expdone->arrive", d(16, 2))
 print("  P0 arrive -> mma sees", d(2, 8), " P1:", d(5, 9))
 print("  mma S0 issued -> sm0 S ready (next tile)", np.median(t[0, 21:101] - t[6, 21:101]))
 print("  fusion K ready->K0 done", d(10, 11), " K0->K1", d(11, 12), " fusion period", np.median(np.diff(t[10, 20:100])))
