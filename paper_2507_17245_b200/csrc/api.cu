@@ -143,7 +143,7 @@ int validate(const da_params* p, bool distr, Plan* P) {
   if (distr) {
     if (G <= 0) return fail(DA_ERR_INVALID, "group_size=%d", G);
     if (p->d % G) return fail(DA_ERR_PRECONDITION, "d %% G* != 0 (d=%d, G*=%d)", p->d, G);
-    if (G != 1 && G != 2 && G != 4) return fail(DA_ERR_PRECONDITION, "G*=%d unsupported (1|2|4)", G);
+    if (G != 1 && G != 2 && G != 4 && G != 8) return fail(DA_ERR_PRECONDITION, "G*=%d unsupported (1|2|4|8)", G);
     if (p->d / G < 16) return fail(DA_ERR_PRECONDITION, "d/G* = %d < 16", p->d / G);
   }
   Plan& q = *P;

@@ -741,6 +741,8 @@ constexpr size_t smem_of() {
     if (d == 128 && G == 2 && HB == 2) MACRO(128, true, 2, 2);                      \
     if (d == 128 && G == 4 && HB == 1) MACRO(128, true, 4, 1);                      \
     if (d == 128 && G == 4 && HB == 2) MACRO(128, true, 4, 2);                      \
+    if (d == 128 && G == 8 && HB == 1) MACRO(128, true, 8, 1);                      \
+    if (d == 128 && G == 8 && HB == 2) MACRO(128, true, 8, 2);                      \
   }
 
 size_t attn_smem_bytes(int d, int G, int HB, int distr) {

@@ -70,6 +70,7 @@ FAKE = ctypes.c_void_p(0x1000)
     (dict(B=0), 1), (dict(N=-1), 1), (dict(H=3, H_kv=2), 1), (dict(dtype=7), 1),
     (dict(causal=2), 1), (dict(d=96), 2), (dict(d=64, G=3), 2), (dict(G=8), 2),
     (dict(block_l=32), 2), (dict(d=64, block_l=64, G=1), 0), (dict(d=128, block_l=64, G=1), 2),
+    (dict(d=128, block_l=128, G=8), 0), (dict(d=128, block_l=64, G=8), 0), (dict(d=128, G=16), 2),
 ])
 def test_validation_before_any_cuda(L, kw, status):
     p = params(**kw)

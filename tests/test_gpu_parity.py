@@ -119,7 +119,7 @@ def test_exact_parity_configs(name):
 @pytest.mark.parametrize("d,block_l,G", [(64, 64, 1), (64, 64, 2), (64, 64, 4), (64, 128, 1),
                                          (64, 128, 2), (64, 128, 4), (128, 128, 1),
                                          (128, 128, 2), (128, 128, 4), (128, 64, 2),
-                                         (128, 64, 4)])
+                                         (128, 64, 4), (128, 128, 8), (128, 64, 8)])
 @pytest.mark.parametrize("causal", [False, True])
 def test_distr_parity_envelope(d, block_l, G, causal):
     # several Q/K tiles plus ragged tails, GQA (H=4 over H_kv=2)
@@ -142,7 +142,7 @@ def test_group_size_one_matches_exact_oracle():
     assert mx <= MAX_ABS and mean <= MEAN_ABS, (mx, mean)
 
 
-@pytest.mark.parametrize("G", [2, 4])
+@pytest.mark.parametrize("G", [2, 4, 8])
 def test_duplicated_columns_match_exact_oracle(G):
     # Eq. 1: G identical copies per group -> DistrAttention == exact attention
     cfg = cfg_small(N=384, d=128, block_l=128, group_size=G)

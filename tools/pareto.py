@@ -1,0 +1,87 @@
+"""the paper's variants as a GPU Pareto sweep — G* x block_l x d, error against
+exact attention and speed against the own exact kernel (the GPU analogue of Tables 3-4 and
+Fig. 9).
+
+    python tools/pareto.py [--steps K] > gpurun_out/pareto.json   (one JSON line per variant)
+
+Error: DistrAttention output vs the exact kernel's output on the same bf16 inputs (both on the
+GPU; the exact kernel itself matches the fp64 oracle to ~2e-3), for i.i.d. N(0,1) inputs and for
+column-clustered Q (the structure LSH grouping is designed for), at B=1 H=8 N=4096. Reported
+as max-abs, mean-abs and relative Frobenius ||O_distr - O_exact|| / ||O_exact||.
+Speed: C4 shape at N=16k (B=1 H=16), CUDA events around the launches inside the C call;
+distr and exact timed alternately in --rounds rounds, medians reported.
+"""
+import argparse, ctypes, json, os, sys
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch
+import paper_2507_17245_b200 as da
+from paper_2507_17245_b200 import _native
+from synth import CONFIGS, make_qkv
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--steps", type=int, default=10)
+ap.add_argument("--warmup", type=int, default=3)
+ap.add_argument("--speed-n", type=int, default=16384)
+ap.add_argument("--rounds", type=int, default=3)
+args = ap.parse_args()
+L = _native.lib()
+
+VARIANTS = [(d, l, g) for d in (64, 128) for l in (64, 128) for g in (1, 2, 4, 8)
+            if d % g == 0 and (128 // l) * d // g in range(16, 129) and (g != 8 or d == 128)]
+
+
+def timed(fn):
+    for _ in range(args.warmup):
+        fn(None)
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
+    for e3 in evs:
+        for e in e3:
+            e.record()
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for e3 in evs:
+        fn(e3)
+    t1.record()
+    torch.cuda.synchronize()
+    return t0.elapsed_time(t1) / args.steps, sum(e[1].elapsed_time(e[2]) for e in evs) / args.steps
+
+
+def run(q, k, v, out, evs, l, g, exact):
+    if evs is not None:
+        L.distr_attn_set_profile_events(*[ctypes.c_void_p(e.cuda_event) for e in evs])
+    if exact:
+        da.exact_attn_fwd_ex(q, k, v, out, block_l=l)
+    else:
+        da.distr_attn_fwd_ex(q, k, v, out, block_l=l, group_size=g)
+
+
+for d, l, g in VARIANTS:
+    rec = {"d": d, "block_l": l, "G": g, "DR": (128 // l) * d // g}
+    base = CONFIGS["C4"].with_(B=1, H=8, H_kv=8, N=4096, d=d, block_l=l, group_size=g)
+    for dist in ("normal", "clustered"):
+        q, k, v = make_qkv(base, device="cuda", dist=dist)
+        o_d = da.distr_attn_fwd_ex(q, k, v, block_l=l, group_size=g).float()
+        o_x = da.exact_attn_fwd_ex(q, k, v, block_l=l).float()
+        diff = (o_d - o_x).abs()
+        rec[f"err_{dist}"] = {"max_abs": diff.max().item(), "mean_abs": diff.mean().item(),
+                              "rel_fro": ((o_d - o_x).norm() / o_x.norm()).item()}
+        del q, k, v
+    c = CONFIGS["C4"].with_(B=1, H=16, H_kv=16, N=args.speed_n, d=d, block_l=l, group_size=g)
+    q, k, v = make_qkv(c, device="cuda")
+    out = torch.empty_like(q)
+    # distr and exact alternate in rounds (clock / power drift hits both alike); medians
+    dd, xx = [], []
+    for _ in range(args.rounds):
+        dd.append(timed(lambda e: run(q, k, v, out, e, l, g, False)))
+        xx.append(timed(lambda e: run(q, k, v, out, e, l, g, True)))
+    d_ms, d_attn = sorted(dd)[len(dd) // 2]
+    x_ms = sorted(xx)[len(xx) // 2][0]
+    pairs = c.B * c.H * c.N * c.N
+    rec.update({"speed_shape": f"B=1 H=16 N={c.N}", "distr_ms": d_ms, "distr_attn_kernel_ms": d_attn,
+                "exact_ms": x_ms, "speedup_vs_exact": x_ms / d_ms,
+                "distr_tflops_executed": pairs * (2 * rec["DR"] + 2 * d) / (d_attn * 1e-3) / 1e12})
+    print(json.dumps(rec), flush=True)
+    del q, k, v, out
+    torch.cuda.empty_cache()
