@@ -104,6 +104,42 @@ int distr_attn_projection(unsigned long long seed, int block_l, float* host_out)
  * (0 if the params are invalid). */
 size_t distr_attn_workspace_size(const da_params* p);
 
+/* Block-size planner: the B200 analogue of "Block size selection" (§3.3.1, Eq. 4-5,
+ * Table 2). Host-only (no CUDA call, no GPU needed). For (N, d, block_l, group_size, distr) it
+ * reports the tiling the attention kernel is compiled with and the quantities the paper's rules
+ * are stated in, re-derived for tcgen05/TMEM/TMA:
+ *   - I/O model (unnumbered equation): I(l, m) = N/l * (l d + 2 N d + l d) elements, i.e.
+ *     each Q block re-reads all of K and V; on B200 the two Q tiles of a CTA share every K/V tile
+ *     and the re-reads across CTAs of a head are served by the 126 MB L2, so HBM sees Q, K, V, O
+ *     about once (plus the K^T layout pass for distr);
+ *   - Eq. 4: l, m multiples of the tensor-core tile N' -> l = UMMA M = 128 rows per Q
+ *     tile (block_l = 64 stacks two hash blocks in one tile), m = UMMA N of S, a multiple of 16
+ *     and <= 256;
+ *   - Eq. 5: enough work per SM to keep the tensor core busy -> two Q tiles per CTA (the
+ *     softmax of one overlaps the MMAs of the other), subject to TMEM (tiles * (d + m) <= 512
+ *     columns) and shared memory (Q/Q̂ tiles + K/V ring + K̂ ring <= 227 KB per CTA).
+ * distr = 0 describes the exact kernel (group_size ignored). Returns DA_OK, DA_ERR_INVALID (NULL
+ * out, N < 1) or DA_ERR_PRECONDITION (combination outside the supported envelope). */
+typedef struct da_plan {
+  int tile_m;            /* query rows per Q tile (UMMA M) */
+  int tiles_per_cta;     /* Q tiles per CTA */
+  int tile_n;            /* keys per K/V tile: m (UMMA N of S, K of PV) */
+  int s_width;           /* contraction width of S: d (exact) or (128 / block_l) * d / G* */
+  int kv_stages;         /* K (or K^T) and V TMA ring depth */
+  int khat_stages;       /* fused K̂^T buffers per Q tile (distr) */
+  int threads;           /* threads per CTA */
+  int smem_bytes;        /* dynamic shared memory per CTA */
+  int tmem_cols;         /* TMEM columns allocated per CTA */
+  int m_max_tmem;        /* largest m (multiple of 16, <= 256) the TMEM budget admits at tiles_per_cta */
+  int ctas;              /* CTAs of one launch for (B*H = 1, N) */
+  double mma_clk_per_tile;   /* ideal tcgen05 clk per 128 x m tile: 2*128*m*(s_width + d) / 8192 */
+  double exp_clk_per_tile;   /* MUFU clk for the tile's 128*m exp2 at 16 per clk per SM */
+  double fusion_smem_bytes_per_tile; /* distr: K^T tile read + K̂^T tile written per (Q tile, K tile) */
+  double hbm_bytes_paper;    /* I(l, m) * 2 bytes for one head (bf16), l = block_l */
+  double hbm_bytes_b200;     /* one head on this kernel: Q + K + V + O (+ K^T write and read, distr) */
+} da_plan;
+int distr_attn_plan(int N, int d, int block_l, int group_size, int distr, da_plan* out);
+
 /* Static description of a status code. */
 const char* distr_attn_status_string(int status);
 

@@ -19,7 +19,7 @@ from ._native import DA_BF16, DA_F32, DaParams, DistrAttnError, check, last_laun
 __all__ = [
     "distr_attn_fwd", "distr_attn_fwd_ex", "exact_attn_fwd_ex", "distr_attn_fwd_host",
     "distr_attn_hash", "distr_attn_projection", "distr_attn_workspace_size", "make_params",
-    "DistrAttnError", "last_launch_count",
+    "DistrAttnError", "last_launch_count", "distr_attn_plan",
 ]
 
 _DT = {torch.bfloat16: DA_BF16, torch.float32: DA_F32}
@@ -146,6 +146,14 @@ def distr_attn_workspace_size(q_shape, kv_heads, *, block_l=128, group_size=2,
     p.B, p.H, p.H_kv, p.N, p.d = B, H, kv_heads, N, d
     p.block_l, p.group_size, p.dtype = block_l, group_size, _DT[dtype]
     return int(_native.lib().distr_attn_workspace_size(ctypes.byref(p)))
+
+
+def distr_attn_plan(N: int, d: int, *, block_l: int = 128, group_size: int = 2, distr: bool = True) -> dict:
+    """Block-size planner (include/distr_attn.h distr_attn_plan; §3.3.1 P:320-369 re-derived for
+    tcgen05/TMEM). Host-only: no GPU needed."""
+    out = _native.DaPlan()
+    check(_native.lib().distr_attn_plan(N, d, block_l, group_size, int(distr), ctypes.byref(out)))
+    return {name: getattr(out, name) for name, _ in _native.DaPlan._fields_}
 
 
 def default_scale(d: int) -> float:

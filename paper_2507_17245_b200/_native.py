@@ -20,7 +20,7 @@ EXPORTED = (
     "distr_attn_init_params", "distr_attn_fwd", "distr_attn_fwd_ex", "distr_attn_fwd_host",
     "exact_attn_fwd_ex", "distr_attn_hash", "distr_attn_projection", "distr_attn_workspace_size",
     "distr_attn_status_string", "distr_attn_last_error", "distr_attn_last_launch_count",
-    "distr_attn_set_profile_events", "distr_attn_set_trace",
+    "distr_attn_set_profile_events", "distr_attn_set_trace", "distr_attn_plan",
 )
 
 
@@ -33,6 +33,14 @@ class DaParams(ctypes.Structure):
         ("workspace_bytes", ctypes.c_size_t), ("lse", ctypes.c_void_p),
         ("bucket_ids", ctypes.c_void_p), ("perm", ctypes.c_void_p),
     ]
+
+
+class DaPlan(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int) for n in (
+        "tile_m", "tiles_per_cta", "tile_n", "s_width", "kv_stages", "khat_stages", "threads",
+        "smem_bytes", "tmem_cols", "m_max_tmem", "ctas")] + [(n, ctypes.c_double) for n in (
+        "mma_clk_per_tile", "exp_clk_per_tile", "fusion_smem_bytes_per_tile", "hbm_bytes_paper",
+        "hbm_bytes_b200")]
 
 
 class DistrAttnError(RuntimeError):
@@ -71,6 +79,7 @@ def lib() -> ctypes.CDLL:
             L.distr_attn_last_launch_count.restype = i32
             L.distr_attn_set_profile_events.argtypes = [vp, vp, vp]
             L.distr_attn_set_trace.argtypes = [vp]
+            L.distr_attn_plan.argtypes = [i32, i32, i32, i32, i32, ctypes.POINTER(DaPlan)]
             _lib = L
     return _lib
 

@@ -450,6 +450,40 @@ size_t distr_attn_workspace_size(const da_params* p) {
   return P.total > E.total ? P.total : E.total;
 }
 
+int distr_attn_plan(int N, int d, int block_l, int group_size, int distr, da_plan* out) {
+  g_last_error.clear();
+  if (!out) return fail(DA_ERR_INVALID, "out is NULL");
+  da_params p;
+  distr_attn_init_params(&p, 1, 1, N, d, block_l, distr ? group_size : 1, 0);
+  Plan P;
+  if (int s = validate(&p, distr != 0, &P)) return s;
+  da::AttnConfig c;
+  if (!da::attn_config(P.d, P.G, P.HB, distr ? 1 : 0, &c))
+    return fail(DA_ERR_PRECONDITION, "no kernel for d=%d G*=%d block_l=%d", P.d, P.G, P.l);
+  *out = da_plan{};
+  out->tile_m = 128;
+  out->tiles_per_cta = 2;
+  out->tile_n = 128;
+  out->s_width = c.dr;
+  out->kv_stages = c.ns;
+  out->khat_stages = c.nkh;
+  out->threads = c.threads;
+  out->smem_bytes = c.smem;
+  out->tmem_cols = 512;  // 2 tiles x (O: d + S: m), rounded up to the allocation granule
+  // Eq. 5 analogue: the largest m with tiles * (d + m) <= 512 TMEM columns
+  int m_max = (512 / out->tiles_per_cta - P.d) / 16 * 16;
+  out->m_max_tmem = m_max > 256 ? 256 : m_max;
+  out->ctas = (P.N + 255) / 256;
+  const double m = out->tile_n;
+  out->mma_clk_per_tile = 2.0 * 128 * m * (c.dr + P.d) / 8192.0;
+  out->exp_clk_per_tile = 128.0 * m / 16.0;
+  out->fusion_smem_bytes_per_tile = distr ? (double)P.d * m * 2 + (double)c.dr * m * 2 : 0.0;
+  const double Nd = (double)P.N * P.d, l = P.l;
+  out->hbm_bytes_paper = 2.0 * ((double)P.N / l) * (l * P.d + 2.0 * Nd + l * P.d);
+  out->hbm_bytes_b200 = 2.0 * 4.0 * Nd + (distr ? 2.0 * 2.0 * Nd : 0.0);
+  return DA_OK;
+}
+
 const char* distr_attn_status_string(int status) {
   switch (status) {
     case DA_OK: return "ok";

@@ -752,6 +752,23 @@ size_t attn_smem_bytes(int d, int G, int HB, int distr) {
   return 0;
 }
 
+template <int D, bool DI, int G, int HB>
+AttnConfig config_of() {
+  using C = Cfg<D, DI, G, HB>;
+  return AttnConfig{C::DR, C::NS, C::NKH, threads_of<DI>(), C::SMEM};
+}
+
+bool attn_config(int d, int G, int HB, int distr, AttnConfig* out) {
+#define DA_CFG(D_, DI_, G_, HB_) \
+  {                              \
+    *out = config_of<D_, DI_, G_, HB_>(); \
+    return true;                 \
+  }
+  DA_DISPATCH(DA_CFG)
+#undef DA_CFG
+  return false;
+}
+
 cudaError_t launch_attn(const AttnLaunch& L, const AttnArgs& a, cudaStream_t st) {
   const int d = L.d, G = L.G, HB = L.HB, distr = L.distr;
   // EMU (pairs of 8 on the FMA pipe): default per flavour, overridable for tuning (DA_EMU env).

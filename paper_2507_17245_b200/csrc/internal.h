@@ -55,5 +55,11 @@ struct AttnLaunch {
 cudaError_t launch_attn(const AttnLaunch& L, const AttnArgs& a, cudaStream_t st);
 // Shared memory bytes the attention kernel uses (0 if unsupported combination).
 size_t attn_smem_bytes(int d, int G, int HB, int distr);
+// Compile-time configuration of the attention kernel for (d, G, HB, distr): S width, ring depths,
+// threads, shared memory. Returns false for an unsupported combination.
+struct AttnConfig {
+  int dr, ns, nkh, threads, smem;
+};
+bool attn_config(int d, int G, int HB, int distr, AttnConfig* out);
 
 }  // namespace da
