@@ -92,6 +92,17 @@ int distr_attn_fwd_host(const void* q, const void* k, const void* v, void* out,
 int exact_attn_fwd_ex(const void* q, const void* k, const void* v, void* out, const da_params* p,
                       void* cuda_stream);
 
+/* DistrAttention with GLOBAL grouping ("a unique grouping strategy over the complete Q
+ * and K^T", which the paper reports as less accurate than block-wise grouping):
+ * one LSH per (b, h) over all N rows (projection 16 x N from (seed, N); reading R17), one
+ * permutation per head, Q̂ and K̂ = grouped sums of K columns materialised once per query head in
+ * the workspace, then attention with S contracted over d/G* and no per-tile fusion. Same
+ * params as distr_attn_fwd_ex except: bf16 only, block_l is not used by the method (tiles are 128
+ * rows) but must be valid, and the optional bucket_ids / perm exports are [B, H, 1, d].
+ * Workspace: distr_attn_workspace_size() covers it. Status codes as distr_attn_fwd_ex. */
+int distr_attn_global_fwd_ex(const void* q, const void* k, const void* v, void* out, const da_params* p,
+                             void* cuda_stream);
+
 /* Run only the LSH step of the prep kernel and export p->bucket_ids and/or p->perm (at least one
  * must be non-NULL). Bit-exact contract with the CPU oracle (fp32 fma chain, ascending rows). */
 int distr_attn_hash(const void* q, const da_params* p, void* cuda_stream);

@@ -25,6 +25,10 @@
  *   oracle_distr_scores — G*=1 == QK^T, duplicated columns exact (Eq. 1), distributive
  *                          identity vs expanded-Q GEMM, d=6 brute force (Eq. 3), Tables 3-4 band.
  *   oracle_attn_items   — torch fp64 SDPA (exact), N=1, S=0 column mean, causal row 0, GQA.
+ *
+ * Global grouping ("a unique grouping strategy over the complete Q and K^T", DESIGN.md
+ * reading R17) needs no separate code: it is this block-wise method with block_l = N (one hash
+ * block spanning every row of the head, projection (seed, N)).
  */
 #include <math.h>
 #include <stdint.h>

@@ -19,7 +19,7 @@ from ._native import DA_BF16, DA_F32, DaParams, DistrAttnError, check, last_laun
 __all__ = [
     "distr_attn_fwd", "distr_attn_fwd_ex", "exact_attn_fwd_ex", "distr_attn_fwd_host",
     "distr_attn_hash", "distr_attn_projection", "distr_attn_workspace_size", "make_params",
-    "DistrAttnError", "last_launch_count", "distr_attn_plan",
+    "DistrAttnError", "last_launch_count", "distr_attn_plan", "distr_attn_global_fwd_ex",
 ]
 
 _DT = {torch.bfloat16: DA_BF16, torch.float32: DA_F32}
@@ -78,6 +78,25 @@ def distr_attn_fwd_ex(q, k, v, out=None, *, block_l=128, group_size=2, seed=0, c
                     v=v, out=out)
     check(_native.lib().distr_attn_fwd_ex(_ptr(q), _ptr(k), _ptr(v), _ptr(out), ctypes.byref(p),
                                           _stream(stream)))
+    return out
+
+
+def distr_attn_global_fwd_ex(q, k, v, out=None, *, group_size=2, seed=0, causal=False, scale=0.0,
+                             lse=None, bucket_ids=None, perm=None, workspace=None, stream=None):
+    """DistrAttention with one grouping per head (global LSH over all N rows, P:306). bf16 only;
+    bucket_ids / perm exports are [B, H, 1, d]. Returns `out`."""
+    _check_tensors(q, k, v, out, lse)
+    B, H, N, d = q.shape
+    for t in (bucket_ids, perm):
+        if t is not None and (t.numel() < B * H * d or not t.is_contiguous()):
+            raise ValueError("bucket_ids / perm exports must be contiguous [B, H, 1, d]")
+    if out is None:
+        out = torch.empty_like(q)
+    p = make_params(q, k, block_l=128, group_size=group_size, seed=seed, causal=causal,
+                    scale=scale, lse=lse, bucket_ids=bucket_ids, perm=perm, workspace=workspace,
+                    v=v, out=out)
+    check(_native.lib().distr_attn_global_fwd_ex(_ptr(q), _ptr(k), _ptr(v), _ptr(out), ctypes.byref(p),
+                                                 _stream(stream)))
     return out
 
 

@@ -21,6 +21,7 @@ EXPORTED = (
     "exact_attn_fwd_ex", "distr_attn_hash", "distr_attn_projection", "distr_attn_workspace_size",
     "distr_attn_status_string", "distr_attn_last_error", "distr_attn_last_launch_count",
     "distr_attn_set_profile_events", "distr_attn_set_trace", "distr_attn_plan",
+    "distr_attn_global_fwd_ex",
 )
 
 
@@ -67,7 +68,8 @@ def lib() -> ctypes.CDLL:
             L.distr_attn_init_params.argtypes = [P, i32, i32, i32, i32, i32, i32, ctypes.c_ulonglong]
             L.distr_attn_fwd.argtypes = [vp, vp, vp, vp, i32, i32, i32, i32, i32, i32,
                                          ctypes.c_ulonglong]
-            for name in ("distr_attn_fwd_ex", "exact_attn_fwd_ex", "distr_attn_fwd_host"):
+            for name in ("distr_attn_fwd_ex", "exact_attn_fwd_ex", "distr_attn_fwd_host",
+                         "distr_attn_global_fwd_ex"):
                 getattr(L, name).argtypes = [vp, vp, vp, vp, P, vp]
             L.distr_attn_hash.argtypes = [vp, P, vp]
             L.distr_attn_projection.argtypes = [ctypes.c_ulonglong, i32, vp]

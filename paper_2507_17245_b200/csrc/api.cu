@@ -345,6 +345,74 @@ int forward(const void* q, const void* k, const void* v, void* out, const da_par
   return DA_OK;
 }
 
+// Workspace of the global-grouping variant: perm [BH][d] u8, Q̂ and K̂ [BH][N][d/G*] bf16.
+size_t global_ws_bytes(const Plan& P, size_t* off_qhat, size_t* off_khat) {
+  const size_t BH = (size_t)P.B * P.H, DR = (size_t)P.d / P.G;
+  size_t o = al256(BH * P.d);
+  *off_qhat = o;
+  o = al256(o + BH * P.N * DR * 2);
+  *off_khat = o;
+  return al256(o + BH * P.N * DR * 2);
+}
+
+int forward_global(const void* q, const void* k, const void* v, void* out, const da_params* p, cudaStream_t st) {
+  Plan P;
+  if (int s = validate(p, true, &P)) return s;
+  if (!q || !k || !v || !out) return fail(DA_ERR_INVALID, "null tensor pointer");
+  if (P.f32) return fail(DA_ERR_PRECONDITION, "global grouping: bf16 inputs only");
+  int dev;
+  if (int s = current_device(&dev)) return s;
+  size_t off_qh, off_kh;
+  const size_t need = global_ws_bytes(P, &off_qh, &off_kh);
+  uint8_t* ws;
+  if (p->workspace) {
+    if (p->workspace_bytes < need)
+      return fail(DA_ERR_PRECONDITION, "workspace too small (%zu < %zu)", p->workspace_bytes, need);
+    ws = static_cast<uint8_t*>(p->workspace);
+  } else {
+    void* w;
+    if (int s = get_pool(g_pool, dev, need, &w)) return s;
+    ws = static_cast<uint8_t*>(w);
+  }
+  const float* proj = nullptr;  // one projection over all N rows: (seed, N) -> [16][N]
+  if (int s = get_projection(dev, p->seed, P.N, st, &proj)) return s;
+  const size_t BH = (size_t)P.B * P.H, BHkv = (size_t)P.B * P.Hkv;
+  const int DR = P.d / P.G;
+  record_ev(0, st);
+  da::GlobalArgs g{};
+  g.q = static_cast<const uint16_t*>(q);
+  g.k = static_cast<const uint16_t*>(k);
+  g.BH = (int)BH; g.H = P.H; g.Hkv = P.Hkv; g.N = P.N; g.d = P.d; g.G = P.G;
+  g.proj = proj;
+  g.perm = ws;
+  g.bucket_out = p->bucket_ids;
+  g.perm_out = p->perm;
+  g.qhat = reinterpret_cast<uint16_t*>(ws + off_qh);
+  g.khat = reinterpret_cast<uint16_t*>(ws + off_kh);
+  DA_CUDA(da::launch_global_prep(g, st));
+  // the exact-flavour kernel with S contracted over DR = d/G* (A = Q̂, B = K̂, both K-major)
+  const int sw = DR * 2 >= 128 ? 128 : DR * 2;
+  CUtensorMap tmA, tmK, tmV;
+  if (int s = make_map(&tmA, g.qhat, DR, P.N, BH, sw / 2, 128, sw)) return s;
+  if (int s = make_map(&tmK, g.khat, DR, P.N, BH, sw / 2, 128, sw)) return s;
+  if (int s = make_map(&tmV, v, P.d, P.N, BHkv, 64, 128, 128)) return s;
+  da::AttnArgs aa{};
+  aa.N = P.N; aa.H = P.H; aa.H_kv = P.Hkv; aa.nqt = P.nqt; aa.nkt = P.nkt; aa.nqb = P.nqb; aa.block_l = P.l;
+  aa.scale_log2 = P.scale * 1.4426950408889634f;
+  aa.causal = P.causal;
+  aa.out = out;
+  aa.lse = p->lse;
+  aa.trace = g_trace;
+  g_trace = nullptr;
+  da::AttnLaunch L{P.d, P.G, 1, 0, (int)BH, &tmA, &tmK, &tmV, default_emu(P, true)};
+  record_ev(1, st);
+  DA_CUDA(da::launch_attn(L, aa, st));
+  record_ev(2, st);
+  g_ev[0] = g_ev[1] = g_ev[2] = nullptr;
+  g_last_launches = 3;
+  return DA_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -376,6 +444,11 @@ int distr_attn_fwd_ex(const void* q, const void* k, const void* v, void* out, co
 int exact_attn_fwd_ex(const void* q, const void* k, const void* v, void* out, const da_params* p,
                       void* cuda_stream) {
   return forward(q, k, v, out, p, static_cast<cudaStream_t>(cuda_stream), false);
+}
+
+int distr_attn_global_fwd_ex(const void* q, const void* k, const void* v, void* out, const da_params* p,
+                             void* cuda_stream) {
+  return forward_global(q, k, v, out, p, static_cast<cudaStream_t>(cuda_stream));
 }
 
 int distr_attn_fwd_host(const void* q, const void* k, const void* v, void* out, const da_params* p,
@@ -447,7 +520,10 @@ size_t distr_attn_workspace_size(const da_params* p) {
   if (validate(p, true, &P)) return 0;
   Plan E;
   validate(p, false, &E);
-  return P.total > E.total ? P.total : E.total;
+  size_t a, b;
+  const size_t gl = P.f32 ? 0 : global_ws_bytes(P, &a, &b);
+  size_t m = P.total > E.total ? P.total : E.total;
+  return m > gl ? m : gl;
 }
 
 int distr_attn_plan(int N, int d, int block_l, int group_size, int distr, da_plan* out) {

@@ -41,14 +41,15 @@ constexpr int kSmemMax = 232448 - 1024;
 
 template <int D, bool DISTR, int G, int HB>
 struct Cfg {
-  static constexpr int DR = DISTR ? HB * D / G : D;  // contraction width of S
+  // contraction width of S: block-wise distr HB*d/G*; exact d (G = 1); global grouping d/G*
+  static constexpr int DR = DISTR ? HB * D / G : D / G;
   static constexpr int A_COLS = DR;
   static constexpr int A_SW = (A_COLS * 2 >= 128) ? 128 : A_COLS * 2;  // swizzle span (bytes)
   static constexpr int A_BOX_COLS = A_SW / 2;
   static constexpr int A_NBOX = A_COLS / A_BOX_COLS;
   static constexpr int A_BOX_BYTES = BM * A_SW;
   static constexpr int A_BYTES = A_NBOX * A_BOX_BYTES;  // one Q tile
-  static constexpr int K_BYTES = BN * D * 2;             // K tile (exact) or K^T tile (distr)
+  static constexpr int K_BYTES = BN * (DISTR ? D : DR) * 2;  // K^T tile (distr), K / K̂ tile (exact/global)
   static constexpr int V_BYTES = BN * D * 2;
   static constexpr int KH_BYTES = DISTR ? DR * BN * 2 : 0;
   static constexpr int al(int x) { return (x + 1023) / 1024 * 1024; }
@@ -368,8 +369,9 @@ __global__ void __launch_bounds__(threads_of<DISTR>(), 1)
         if (DISTR) {
           tma_load_3d(sK + s * C::K_BYTES, &tmK, &bars[B_KFULL + s], i * BN, 0, bhkv);
         } else {
-          for (int bx = 0; bx < D / 64; ++bx)
-            tma_load_3d(sK + s * C::K_BYTES + bx * (BN * 128), &tmK, &bars[B_KFULL + s], bx * 64, i * BN, bhkv);
+          for (int bx = 0; bx < C::A_NBOX; ++bx)  // K (G = 1) or K̂ of this query head (global)
+            tma_load_3d(sK + s * C::K_BYTES + bx * C::A_BOX_BYTES, &tmK, &bars[B_KFULL + s], bx * C::A_BOX_COLS,
+                        i * BN, G > 1 ? bh : bhkv);
         }
       }
     }
@@ -411,8 +413,8 @@ __global__ void __launch_bounds__(threads_of<DISTR>(), 1)
             bdesc = make_sdesc(smem_u32(sKh + (t * NKH + i % NKH) * C::KH_BYTES) + kk * 2048, C::DR * 128, 1024,
                                kSw128);
           } else {
-            bdesc = make_sdesc(smem_u32(sK + s * C::K_BYTES) + (kk / 4) * (BN * 128) + (kk % 4) * 32, 16, 1024,
-                               kSw128);
+            bdesc = make_sdesc(smem_u32(sK + s * C::K_BYTES) + (kk / kpb) * C::A_BOX_BYTES + (kk % kpb) * 32, 16,
+                               8 * C::A_SW, C::A_LAYOUT);
           }
           mma_ss(d_s, adesc, bdesc, IDESC_S, kk > 0 ? 1u : 0u);
         }
@@ -727,8 +729,13 @@ constexpr size_t smem_of() {
 
 #define DA_DISPATCH(MACRO)                                                          \
   if (!distr) {                                                                     \
-    if (d == 64) MACRO(64, false, 1, 1);                                            \
-    if (d == 128) MACRO(128, false, 1, 1);                                          \
+    if (d == 64 && G == 1) MACRO(64, false, 1, 1);                                  \
+    if (d == 64 && G == 2) MACRO(64, false, 2, 1);                                  \
+    if (d == 64 && G == 4) MACRO(64, false, 4, 1);                                  \
+    if (d == 128 && G == 1) MACRO(128, false, 1, 1);                                \
+    if (d == 128 && G == 2) MACRO(128, false, 2, 1);                                \
+    if (d == 128 && G == 4) MACRO(128, false, 4, 1);                                \
+    if (d == 128 && G == 8) MACRO(128, false, 8, 1);                                \
   } else {                                                                          \
     if (d == 64 && G == 1 && HB == 1) MACRO(64, true, 1, 1);                        \
     if (d == 64 && G == 1 && HB == 2) MACRO(64, true, 1, 2);                        \

@@ -41,6 +41,21 @@ struct AttnArgs {
 };
 
 cudaError_t launch_prep(const PrepArgs& a, cudaStream_t st);
+
+// Global-grouping variant (prep_global.cu): one LSH per head over all N rows, then Q̂ and K̂
+// materialised per query head. All pointers are device pointers; q, k bf16.
+struct GlobalArgs {
+  const uint16_t* q;     // [BH][N][d]
+  const uint16_t* k;     // [BHkv][N][d]
+  int BH, H, Hkv, N, d, G;
+  const float* proj;     // [16][N] (seed, N)
+  uint8_t* perm;         // [BH][d] workspace
+  uint16_t* bucket_out;  // optional export [BH][d]
+  uint8_t* perm_out;     // optional export [BH][d]
+  uint16_t* qhat;        // [BH][N][d/G]
+  uint16_t* khat;        // [BH][N][d/G]
+};
+cudaError_t launch_global_prep(const GlobalArgs& a, cudaStream_t st);
 cudaError_t launch_convert_bf16(const float* src, uint16_t* dst, size_t n, cudaStream_t st);
 
 // Which kernel flavour: DISTR with (d, G, HB) or exact with d.

@@ -96,6 +96,19 @@ def _draw(cfg: Config, dist: str, g: torch.Generator, device):
         q = centres[..., assign] + 0.1 * torch.randn(shp_q, generator=g, device=device)
         return (q, torch.randn(shp_kv, generator=g, device=device),
                 torch.randn(shp_kv, generator=g, device=device))
+    if dist == "block_clustered":
+        # column clusters that change every 128 rows (one assignment per 128-row Q block): the
+        # structure per-block grouping can follow and one grouping per head cannot
+        nc = max(1, cfg.d // 4)
+        centres = torch.randn((cfg.H, cfg.N, nc), generator=g, device=device)
+        nb = (cfg.N + 127) // 128
+        assign = torch.randint(0, nc, (nb, cfg.d), generator=g, device=device)
+        rows = torch.arange(cfg.N, device=device) // 128
+        idx = assign[rows]  # [N, d]
+        q = torch.gather(centres, 2, idx.unsqueeze(0).expand(cfg.H, -1, -1))
+        q = q + 0.1 * torch.randn(shp_q, generator=g, device=device)
+        return (q, torch.randn(shp_kv, generator=g, device=device),
+                torch.randn(shp_kv, generator=g, device=device))
     raise ValueError(f"unknown dist {dist!r}")
 
 

@@ -1,0 +1,104 @@
+"""GPU parity of the global-grouping variant (distr_attn_global_fwd_ex, reading R17):
+one LSH block spanning all N rows of a head. The oracle computes it as block-wise DistrAttention
+with block_l = N (same projection (seed, N), same fp32 fma chain, one permutation per head).
+
+Bar: bucket ids / permutations bit-exact; outputs within max-abs 2e-2 and mean-abs 2e-3.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import paper_2507_17245_b200 as da
+from gpu_util import MAX_ABS, MEAN_ABS, errors, gather_items, oracle_items, to_np32
+from synth import Config, make_qkv
+
+pytestmark = pytest.mark.gpu
+DEV = "cuda"
+
+
+def cfg(**kw):
+    base = dict(name="g", B=1, H=2, H_kv=2, N=300, d=128, block_l=128, group_size=2, causal=False,
+                dtype="bf16", data_seed=7)
+    base.update(kw)
+    return Config(**base)
+
+
+def run_global(c: Config, *, dist="normal", seed=3, q=None, k=None, v=None, oracle_G=None):
+    if q is None:
+        q, k, v = make_qkv(c, dist=dist, device=DEV)
+    B, H = c.B, c.H
+    bk = torch.zeros((B, H, 1, c.d), dtype=torch.int16, device=DEV)
+    pm = torch.zeros((B, H, 1, c.d), dtype=torch.uint8, device=DEV)
+    out = da.distr_attn_global_fwd_ex(q, k, v, group_size=c.group_size, seed=seed, causal=c.causal,
+                                      bucket_ids=bk, perm=pm)
+    torch.cuda.synchronize()
+    # hashing: bit-exact against the oracle's single block of height N
+    ob, op = oracle.hash_all(to_np32(q), c.N, seed)
+    assert np.array_equal(bk.cpu().numpy().view(np.uint16), ob)
+    assert np.array_equal(pm.cpu().numpy(), op)
+    items = [(bh, 0) for bh in range(B * H)]
+    G = c.group_size if oracle_G is None else oracle_G
+    want = oracle_items(q, k, v, items, block_l=c.N, G=G, seed=seed, causal=c.causal)
+    got = gather_items(out, items, c.N)
+    assert np.isfinite(got).all()
+    return errors(got, want)
+
+
+@pytest.mark.parametrize("d,G", [(64, 1), (64, 2), (64, 4), (128, 1), (128, 2), (128, 4), (128, 8)])
+@pytest.mark.parametrize("causal", [False, True])
+def test_global_parity(d, G, causal):
+    mx, mean = run_global(cfg(B=2, H=4, H_kv=2, N=333, d=d, group_size=G, causal=causal))
+    assert mx <= MAX_ABS and mean <= MEAN_ABS, (mx, mean)
+
+
+@pytest.mark.parametrize("N", [1, 2, 127, 128, 129, 700])
+def test_global_ragged_lengths(N):
+    mx, mean = run_global(cfg(N=N))
+    assert mx <= MAX_ABS and mean <= MEAN_ABS, (N, mx, mean)
+
+
+def test_global_hash_long_sequence():
+    # the fp32 chain runs over all N rows in one thread: still bit-exact at N = 4096
+    c = cfg(N=4096, H=2)
+    q, _, _ = make_qkv(c, device=DEV)
+    bk = torch.zeros((1, 2, 1, 128), dtype=torch.int16, device=DEV)
+    pm = torch.zeros((1, 2, 1, 128), dtype=torch.uint8, device=DEV)
+    da.distr_attn_global_fwd_ex(q, q, q, group_size=2, seed=9, bucket_ids=bk, perm=pm)
+    torch.cuda.synchronize()
+    ob, op = oracle.hash_all(to_np32(q), 4096, 9)
+    assert np.array_equal(bk.cpu().numpy().view(np.uint16), ob)
+    assert np.array_equal(pm.cpu().numpy(), op)
+
+
+def test_global_group_size_one_is_exact():
+    mx, mean = run_global(cfg(N=300, group_size=1, causal=True), oracle_G=0)
+    assert mx <= MAX_ABS and mean <= MEAN_ABS, (mx, mean)
+
+
+@pytest.mark.parametrize("G", [2, 4, 8])
+def test_global_duplicated_columns_are_exact(G):
+    # Eq. 1 with one grouping per head: G identical copies per group -> exact attention
+    c = cfg(N=384, group_size=G)
+    g = torch.Generator(device=DEV).manual_seed(3)
+    base = torch.randn((1, 2, 384, 128 // G), generator=g, device=DEV)
+    q = base.repeat_interleave(G, dim=-1).bfloat16().contiguous()
+    k = torch.randn((1, 2, 384, 128), generator=g, device=DEV).bfloat16()
+    v = torch.randn((1, 2, 384, 128), generator=g, device=DEV).bfloat16()
+    mx, mean = run_global(c, q=q, k=k, v=v, oracle_G=0)
+    assert mx <= MAX_ABS and mean <= MEAN_ABS, (mx, mean)
+
+
+def test_blockwise_grouping_is_more_accurate_than_global():
+    # "Applying multiple permutations results in a lower error compared to using a unique
+    # grouping strategy over the complete Q and K^T" — on column-clustered Q whose clusters change
+    # from block to block (synth "block_clustered": the structure per-block grouping can follow
+    # and one grouping per head cannot), at N = 2048
+    c = cfg(N=2048, H=4, H_kv=4)
+    q, k, v = make_qkv(c, dist="block_clustered", device=DEV)
+    ex = da.exact_attn_fwd_ex(q, k, v).float()
+    bw = da.distr_attn_fwd_ex(q, k, v, block_l=128, group_size=2).float()
+    gl = da.distr_attn_global_fwd_ex(q, k, v, group_size=2).float()
+    e_bw = ((bw - ex).norm() / ex.norm()).item()
+    e_gl = ((gl - ex).norm() / ex.norm()).item()
+    assert e_bw < e_gl, (e_bw, e_gl)

@@ -4,9 +4,11 @@ Fig. 9, P:468-498, P:712-720).
 
     python tools/pareto.py [--steps K] > gpurun_out/pareto.json   (one JSON line per variant)
 
-Error: DistrAttention output vs the exact kernel's output on the same bf16 inputs (both on the
-GPU; the exact kernel itself matches the fp64 oracle to ~2e-3), for i.i.d. N(0,1) inputs and for
-column-clustered Q (the structure LSH grouping is designed for), at B=1 H=8 N=4096. Reported
+Variants: block-wise (block_l in {64, 128}) and global grouping (one LSH per head over all N
+rows; "block_l": "global"). Error: DistrAttention output vs the exact kernel's output on
+the same bf16 inputs (both on the GPU; the exact kernel itself matches the fp64 oracle to
+~2e-3), for i.i.d. N(0,1) inputs, column-clustered Q (the structure LSH grouping is designed
+for) and block-clustered Q (clusters change every 128 rows), at B=1 H=8 N=4096. Reported
 as max-abs, mean-abs and relative Frobenius ||O_distr - O_exact|| / ||O_exact||.
 Speed: C4 shape at N=16k (B=1 H=16), CUDA events around the launches inside the C call;
 distr and exact timed alternately in --rounds rounds, medians reported.
@@ -29,6 +31,9 @@ L = _native.lib()
 
 VARIANTS = [(d, l, g) for d in (64, 128) for l in (64, 128) for g in (1, 2, 4, 8)
             if d % g == 0 and (128 // l) * d // g in range(16, 129) and (g != 8 or d == 128)]
+# global grouping (one LSH over all N rows per head): block_l = 0 marks it
+VARIANTS += [(d, 0, g) for d in (64, 128) for g in (2, 4, 8) if d // g >= 16]
+DISTS = ("normal", "clustered", "block_clustered")
 
 
 def timed(fn):
@@ -52,23 +57,27 @@ def run(q, k, v, out, evs, l, g, exact):
     if evs is not None:
         L.distr_attn_set_profile_events(*[ctypes.c_void_p(e.cuda_event) for e in evs])
     if exact:
-        da.exact_attn_fwd_ex(q, k, v, out, block_l=l)
+        da.exact_attn_fwd_ex(q, k, v, out, block_l=l or 128)
+    elif l == 0:
+        da.distr_attn_global_fwd_ex(q, k, v, out, group_size=g)
     else:
         da.distr_attn_fwd_ex(q, k, v, out, block_l=l, group_size=g)
 
 
 for d, l, g in VARIANTS:
-    rec = {"d": d, "block_l": l, "G": g, "DR": (128 // l) * d // g}
-    base = CONFIGS["C4"].with_(B=1, H=8, H_kv=8, N=4096, d=d, block_l=l, group_size=g)
-    for dist in ("normal", "clustered"):
+    rec = {"d": d, "block_l": l if l else "global", "G": g, "DR": (128 // (l or 128)) * d // g}
+    base = CONFIGS["C4"].with_(B=1, H=8, H_kv=8, N=4096, d=d, block_l=l or 128, group_size=g)
+    for dist in DISTS:
         q, k, v = make_qkv(base, device="cuda", dist=dist)
-        o_d = da.distr_attn_fwd_ex(q, k, v, block_l=l, group_size=g).float()
-        o_x = da.exact_attn_fwd_ex(q, k, v, block_l=l).float()
+        o_d = torch.empty_like(q)
+        run(q, k, v, o_d, None, l, g, False)
+        o_d = o_d.float()
+        o_x = da.exact_attn_fwd_ex(q, k, v).float()
         diff = (o_d - o_x).abs()
         rec[f"err_{dist}"] = {"max_abs": diff.max().item(), "mean_abs": diff.mean().item(),
                               "rel_fro": ((o_d - o_x).norm() / o_x.norm()).item()}
         del q, k, v
-    c = CONFIGS["C4"].with_(B=1, H=16, H_kv=16, N=args.speed_n, d=d, block_l=l, group_size=g)
+    c = CONFIGS["C4"].with_(B=1, H=16, H_kv=16, N=args.speed_n, d=d, block_l=l or 128, group_size=g)
     q, k, v = make_qkv(c, device="cuda")
     out = torch.empty_like(q)
     # distr and exact alternate in rounds (clock / power drift hits both alike); medians
