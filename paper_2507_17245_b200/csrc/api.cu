@@ -400,6 +400,7 @@ int forward_global(const void* q, const void* k, const void* v, void* out, const
   aa.N = P.N; aa.H = P.H; aa.H_kv = P.Hkv; aa.nqt = P.nqt; aa.nkt = P.nkt; aa.nqb = P.nqb; aa.block_l = P.l;
   aa.scale_log2 = P.scale * 1.4426950408889634f;
   aa.causal = P.causal;
+  aa.k_per_qhead = 1;  // K̂ is materialised per query head
   aa.out = out;
   aa.lse = p->lse;
   aa.trace = g_trace;

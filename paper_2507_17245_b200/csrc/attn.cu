@@ -371,7 +371,7 @@ __global__ void __launch_bounds__(threads_of<DISTR>(), 1)
         } else {
           for (int bx = 0; bx < C::A_NBOX; ++bx)  // K (G = 1) or K̂ of this query head (global)
             tma_load_3d(sK + s * C::K_BYTES + bx * C::A_BOX_BYTES, &tmK, &bars[B_KFULL + s], bx * C::A_BOX_COLS,
-                        i * BN, G > 1 ? bh : bhkv);
+                        i * BN, args.k_per_qhead ? bh : bhkv);
         }
       }
     }

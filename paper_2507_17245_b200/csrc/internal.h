@@ -29,6 +29,7 @@ struct AttnArgs {
   int N, H, H_kv, nqt, nkt, nqb, block_l;
   float scale_log2;  // scale * log2(e)
   int causal;
+  int k_per_qhead;      // exact flavour: K (K̂ of the global variant) indexed by the query head
   const uint8_t* perm;  // [BH][nqb][d] precomputed permutations (distr, fp32 inputs) or NULL:
                         // NULL = the attention CTA hashes its own Q blocks (bf16 inputs)
   const float* proj;    // [16][block_l] projection matrix (distr, in-kernel hashing)
