@@ -62,6 +62,13 @@ typedef struct da_params {
   float* lse;                  /* optional [B, H, N] fp32 natural-log sum-exp of scaled scores */
   unsigned short* bucket_ids;  /* optional [B, H, ceil(N/l), d] uint16 LSH bucket ids (tests) */
   unsigned char* perm;         /* optional [B, H, ceil(N/l), d] uint8 stable sort permutation */
+  int q_shard_offset;          /* Q-block (sequence) sharding: with stride S > 0 */
+  int q_shard_stride;          /* this call computes only the 256-row Q tile pairs dealt to rank
+                                  `offset` of S in a zigzag: slot x*S + offset for even rounds x,
+                                  x*S + S-1-offset for odd x (slots are visited heaviest-first when
+                                  causal, so the split balances causal work). 0 / 0 (the defaults)
+                                  = all pairs. Rows outside the shard are not written (out, lse).
+                                  Requires 0 <= offset < stride when stride > 0. */
 } da_params;
 
 /* Fill `p` with defaults: H_kv = H, non-causal, bf16, scale = 1/sqrt(d), library workspace,

@@ -31,7 +31,7 @@ def _ptr(t):
 
 def make_params(q: torch.Tensor, k: torch.Tensor, *, block_l: int, group_size: int, seed: int = 0,
                 causal: bool = False, scale: float = 0.0, lse=None, bucket_ids=None, perm=None,
-                workspace=None, v=None, out=None) -> DaParams:
+                workspace=None, v=None, out=None, q_shard=None) -> DaParams:
     if q.dim() != 4 or k.dim() != 4:
         raise ValueError("q must be [B,H,N,d] and k/v [B,H_kv,N,d]")
     if k.shape[0] != q.shape[0] or k.shape[2:] != q.shape[2:] or k.dtype != q.dtype:
@@ -52,6 +52,8 @@ def make_params(q: torch.Tensor, k: torch.Tensor, *, block_l: int, group_size: i
     p.lse = None if lse is None else lse.data_ptr()
     p.bucket_ids = None if bucket_ids is None else bucket_ids.data_ptr()
     p.perm = None if perm is None else perm.data_ptr()
+    if q_shard is not None:  # (offset, stride): Q-tile-pair sharding (shard.q_pair_shard)
+        p.q_shard_offset, p.q_shard_stride = int(q_shard[0]), int(q_shard[1])
     return p
 
 
@@ -68,21 +70,23 @@ def _stream(stream):
 
 
 def distr_attn_fwd_ex(q, k, v, out=None, *, block_l=128, group_size=2, seed=0, causal=False,
-                      scale=0.0, lse=None, bucket_ids=None, perm=None, workspace=None, stream=None):
+                      scale=0.0, lse=None, bucket_ids=None, perm=None, workspace=None, stream=None,
+                      q_shard=None):
     """DistrAttention forward (device tensors, current torch stream). Returns `out`."""
     _check_tensors(q, k, v, out, lse)
     if out is None:
         out = torch.empty_like(q)
     p = make_params(q, k, block_l=block_l, group_size=group_size, seed=seed, causal=causal,
                     scale=scale, lse=lse, bucket_ids=bucket_ids, perm=perm, workspace=workspace,
-                    v=v, out=out)
+                    v=v, out=out, q_shard=q_shard)
     check(_native.lib().distr_attn_fwd_ex(_ptr(q), _ptr(k), _ptr(v), _ptr(out), ctypes.byref(p),
                                           _stream(stream)))
     return out
 
 
 def distr_attn_global_fwd_ex(q, k, v, out=None, *, group_size=2, seed=0, causal=False, scale=0.0,
-                             lse=None, bucket_ids=None, perm=None, workspace=None, stream=None):
+                             lse=None, bucket_ids=None, perm=None, workspace=None, stream=None,
+                             q_shard=None):
     """DistrAttention with one grouping per head (global LSH over all N rows, P:306). bf16 only;
     bucket_ids / perm exports are [B, H, 1, d]. Returns `out`."""
     _check_tensors(q, k, v, out, lse)
@@ -94,20 +98,20 @@ def distr_attn_global_fwd_ex(q, k, v, out=None, *, group_size=2, seed=0, causal=
         out = torch.empty_like(q)
     p = make_params(q, k, block_l=128, group_size=group_size, seed=seed, causal=causal,
                     scale=scale, lse=lse, bucket_ids=bucket_ids, perm=perm, workspace=workspace,
-                    v=v, out=out)
+                    v=v, out=out, q_shard=q_shard)
     check(_native.lib().distr_attn_global_fwd_ex(_ptr(q), _ptr(k), _ptr(v), _ptr(out), ctypes.byref(p),
                                                  _stream(stream)))
     return out
 
 
 def exact_attn_fwd_ex(q, k, v, out=None, *, block_l=128, causal=False, scale=0.0, lse=None,
-                      workspace=None, stream=None):
+                      workspace=None, stream=None, q_shard=None):
     """Exact attention on the same sm_100a tiling (reference point). Returns `out`."""
     _check_tensors(q, k, v, out, lse)
     if out is None:
         out = torch.empty_like(q)
     p = make_params(q, k, block_l=block_l, group_size=1, causal=causal, scale=scale, lse=lse,
-                    workspace=workspace, v=v, out=out)
+                    workspace=workspace, v=v, out=out, q_shard=q_shard)
     check(_native.lib().exact_attn_fwd_ex(_ptr(q), _ptr(k), _ptr(v), _ptr(out), ctypes.byref(p),
                                           _stream(stream)))
     return out

@@ -33,6 +33,7 @@ class DaParams(ctypes.Structure):
         ("dtype", ctypes.c_int), ("workspace", ctypes.c_void_p),
         ("workspace_bytes", ctypes.c_size_t), ("lse", ctypes.c_void_p),
         ("bucket_ids", ctypes.c_void_p), ("perm", ctypes.c_void_p),
+        ("q_shard_offset", ctypes.c_int), ("q_shard_stride", ctypes.c_int),
     ]
 
 

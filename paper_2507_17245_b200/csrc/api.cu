@@ -120,6 +120,7 @@ int get_pool(std::map<int, Pool>& pools, int dev, size_t need, void** out) {
 // ---------------------------------------------------------------------------- plan
 struct Plan {
   int B, H, Hkv, N, d, l, G, HB, DR, nqb, nqt, nkt, N_pad, f32, causal;
+  int pair_off, pair_stride;  // Q-tile-pair shard (stride 1 = all pairs)
   float scale;
   size_t off_perm, off_qhat, off_kt, off_qc, off_kc, off_vc, total;
 };
@@ -158,6 +159,11 @@ int validate(const da_params* p, bool distr, Plan* P) {
   q.N_pad = (q.N + 7) / 8 * 8;
   q.f32 = p->dtype == DA_F32;
   q.causal = p->causal;
+  if (p->q_shard_stride < 0 || (p->q_shard_stride == 0 && p->q_shard_offset != 0) ||
+      (p->q_shard_stride > 0 && (p->q_shard_offset < 0 || p->q_shard_offset >= p->q_shard_stride)))
+    return fail(DA_ERR_INVALID, "q shard offset %d / stride %d", p->q_shard_offset, p->q_shard_stride);
+  q.pair_off = p->q_shard_offset;
+  q.pair_stride = p->q_shard_stride > 0 ? p->q_shard_stride : 1;
   q.scale = p->scale > 0.f ? p->scale : (float)(1.0 / std::sqrt((double)q.d));
   const size_t BH = (size_t)q.B * q.H, BHkv = (size_t)q.B * q.Hkv;
   size_t o = 0;
@@ -324,6 +330,7 @@ int forward(const void* q, const void* k, const void* v, void* out, const da_par
 
   da::AttnArgs aa{};
   aa.N = P.N; aa.H = P.H; aa.H_kv = P.Hkv; aa.nqt = P.nqt; aa.nkt = P.nkt; aa.nqb = P.nqb; aa.block_l = P.l;
+  aa.pair_offset = P.pair_off; aa.pair_stride = P.pair_stride;
   aa.scale_log2 = P.scale * 1.4426950408889634f;
   aa.causal = P.causal;
   aa.perm = (distr && P.f32) ? ws + P.off_perm : nullptr;
@@ -398,6 +405,7 @@ int forward_global(const void* q, const void* k, const void* v, void* out, const
   if (int s = make_map(&tmV, v, P.d, P.N, BHkv, 64, 128, 128)) return s;
   da::AttnArgs aa{};
   aa.N = P.N; aa.H = P.H; aa.H_kv = P.Hkv; aa.nqt = P.nqt; aa.nkt = P.nkt; aa.nqb = P.nqb; aa.block_l = P.l;
+  aa.pair_offset = P.pair_off; aa.pair_stride = P.pair_stride;
   aa.scale_log2 = P.scale * 1.4426950408889634f;
   aa.causal = P.causal;
   aa.k_per_qhead = 1;  // K̂ is materialised per query head

@@ -276,8 +276,13 @@ __global__ void __launch_bounds__(threads_of<DISTR>(), 1)
   long long* const trace = (args.trace && blockIdx.x == 0 && blockIdx.y == 0) ? args.trace : nullptr;
 #define DA_TRACE(slot, idx, cond) \
   if (trace && (cond)) trace[(slot) * 256 + ((idx) & 255)] = clock64();
-  // causal: heaviest pairs of Q tiles first
-  const int pair = args.causal ? ((args.nqt + 1) / 2 - 1 - (int)blockIdx.x) : (int)blockIdx.x;
+  // Slot of this CTA. Q-block sharding: round x of a zigzag over `stride` ranks (rank `offset`
+  // takes slot offset in even rounds, stride-1-offset in odd ones); causal: heaviest pairs first.
+  const int npairs = (args.nqt + 1) / 2;
+  const int rx = (int)blockIdx.x;
+  const int slot = rx * args.pair_stride + ((rx & 1) ? args.pair_stride - 1 - args.pair_offset : args.pair_offset);
+  if (slot >= npairs) return;  // past the end in the last round of this shard
+  const int pair = args.causal ? (npairs - 1 - slot) : slot;
   const int b = bh / args.H, h = bh % args.H;
   const int bhkv = b * args.H_kv + h / (args.H / args.H_kv);
   const int qt0 = 2 * pair;
@@ -715,7 +720,8 @@ cudaError_t launch_one(const AttnLaunch& L, const AttnArgs& a, cudaStream_t st) 
   auto kern = attn_kernel<D, DISTR, G, HB, EMU>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
   if (e != cudaSuccess) return e;
-  dim3 grid((a.nqt + 1) / 2, L.BH);
+  const int npairs = (a.nqt + 1) / 2;
+  dim3 grid((npairs + a.pair_stride - 1) / a.pair_stride, L.BH);  // rounds of the zigzag
   kern<<<grid, threads_of<DISTR>(), C::SMEM, st>>>(*L.tmA, *L.tmK, *L.tmV, a);
   return cudaGetLastError();
 }

@@ -27,6 +27,7 @@ struct PrepArgs {
 // Everything the attention kernel needs besides its three TMA descriptors.
 struct AttnArgs {
   int N, H, H_kv, nqt, nkt, nqb, block_l;
+  int pair_offset, pair_stride;  // Q-tile-pair shard: CTA x computes slot offset + x * stride
   float scale_log2;  // scale * log2(e)
   int causal;
   int k_per_qhead;      // exact flavour: K (K̂ of the global variant) indexed by the query head

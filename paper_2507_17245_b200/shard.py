@@ -27,3 +27,58 @@ def max_over_ranks(values, device=None):
     t = torch.tensor([float(x) for x in values], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return t.tolist()
+
+
+# ---------------------------------------------------------------------------------------------
+# Q-block (sequence) sharding — SURVEY §8(e) NEXT / §8(f) row 3: when B·H is smaller than the
+# number of GPUs (long single-head runs), ranks split the 256-row Q tile pairs of every head
+# instead of the heads. Every rank needs all of K and V (one all_gather if they arrive sharded
+# along N); the attention itself has no collective. Slots are dealt in a zigzag (round x: rank
+# takes slot x*world + rank for even x, x*world + world-1-rank for odd x); the kernel visits
+# slots heaviest-first when causal, so every rank gets a near-equal share of the causal work.
+
+TILE_PAIR_ROWS = 256
+
+
+def q_pair_shard(rank: int, world: int) -> tuple[int, int]:
+    """(offset, stride) for da_params.q_shard_offset / q_shard_stride."""
+    if world <= 0 or not 0 <= rank < world:
+        raise ValueError(f"bad rank {rank} / world {world}")
+    return rank, world
+
+
+def q_rows_of_shard(N: int, rank: int, world: int, causal: bool = False) -> list[tuple[int, int]]:
+    """Row ranges [r0, r1) of Q whose outputs `rank` computes (mirrors the kernel's slot -> tile
+    pair mapping: pair = slot, or npairs - 1 - slot when causal)."""
+    npairs = -(-N // TILE_PAIR_ROWS)
+    off, stride = q_pair_shard(rank, world)
+    rows = []
+    for x in range(-(-npairs // stride)):
+        slot = x * stride + (stride - 1 - off if x & 1 else off)
+        if slot >= npairs:
+            continue
+        pair = npairs - 1 - slot if causal else slot
+        rows.append((pair * TILE_PAIR_ROWS, min(N, (pair + 1) * TILE_PAIR_ROWS)))
+    return sorted(rows)
+
+
+def causal_work_of_shard(N: int, rank: int, world: int) -> int:
+    """Number of (query tile, key tile) 128x128 steps `rank` runs for a causal problem."""
+    work = 0
+    for r0, r1 in q_rows_of_shard(N, rank, world, causal=True):
+        for qt in range(r0 // 128, -(-r1 // 128)):
+            work += qt + 1
+    return work
+
+
+def gather_kv_sequence_shards(k_local, v_local, group=None):
+    """all_gather K/V shards split along N (dim 2) -> full K, V on every rank (the one exchange
+    step of Q-block sharding; outside the attention kernel)."""
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    ks = [torch.empty_like(k_local) for _ in range(world)]
+    vs = [torch.empty_like(v_local) for _ in range(world)]
+    dist.all_gather(ks, k_local.contiguous(), group=group)
+    dist.all_gather(vs, v_local.contiguous(), group=group)
+    return torch.cat(ks, dim=2).contiguous(), torch.cat(vs, dim=2).contiguous()
