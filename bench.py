@@ -164,6 +164,8 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu", action="store_true")
     ap.add_argument("--no-parity", action="store_true")
+    ap.add_argument("--shard", default="bh", choices=["bh", "q"],
+                    help="N>1: split (b,h) problems (default) or the Q tile pairs of every head")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
     cfg = CONFIGS[args.config]
@@ -179,8 +181,13 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
-    from paper_2507_17245_b200.shard import batch_shard, max_over_ranks
-    b0, B = batch_shard(cfg.B, rank, world)
+    from paper_2507_17245_b200.shard import batch_shard, max_over_ranks, q_pair_shard, q_rows_of_shard
+    if args.shard == "q":  # every rank holds the whole batch and computes its Q tile pairs
+        b0, B = 0, cfg.B
+        qsh = q_pair_shard(rank, world) if world > 1 else None
+    else:
+        b0, B = batch_shard(cfg.B, rank, world)
+        qsh = None
     G = cfg.group_size
     q, k, v = make_qkv(cfg, device=dev, B=B, head_offset=b0)
     out = torch.empty_like(q)
@@ -198,10 +205,10 @@ def main():
         if evs is not None:
             L.distr_attn_set_profile_events(*[ctypes.c_void_p(e.cuda_event) for e in evs])
         if exact:
-            da.exact_attn_fwd_ex(q, k, v, out, block_l=cfg.block_l, causal=cfg.causal)
+            da.exact_attn_fwd_ex(q, k, v, out, block_l=cfg.block_l, causal=cfg.causal, q_shard=qsh)
         else:
             da.distr_attn_fwd_ex(q, k, v, out, block_l=cfg.block_l, group_size=G, seed=0,
-                                 causal=cfg.causal, workspace=ws)
+                                 causal=cfg.causal, workspace=ws, q_shard=qsh)
 
     def timed(exact):
         for _ in range(args.warmup):
@@ -230,9 +237,11 @@ def main():
     ex_ms, ex_attn_ms, _, _, _ = timed(True)
 
     peaks, peak_src = load_peaks()
+    # FLOPs of this rank's share (whole job / world in both sharding modes)
     exec_f, full_f = flops(cfg, B, G)
-    exec_f_ex, _ = flops(cfg, B, 1)
     exec_f_ex = B * cfg.H * cfg.N * cfg.N * 4 * cfg.d * (0.5 if cfg.causal else 1.0)
+    if args.shard == "q":
+        exec_f, full_f, exec_f_ex = exec_f / world, full_f / world, exec_f_ex / world
     peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
     achieved = exec_f / (attn_ms * 1e-3) / 1e12
     traffic = None
@@ -252,6 +261,10 @@ def main():
         torch.cuda.synchronize()
         scfg = cfg.with_(B=B)
         items = sample_items(scfg, n_heads=2, per_head=2)
+        if qsh is not None:  # only blocks of rank 0's shard were computed here
+            own = q_rows_of_shard(cfg.N, 0, world, cfg.causal)
+            items = [(bh, qb) for bh, _ in items[:1] for r0, r1 in own[:2]
+                     for qb in (r0 // cfg.block_l,)]
         want = oracle_items(q, k, v, items, block_l=cfg.block_l, G=G, causal=cfg.causal)
         got = gather_items(out, items, cfg.block_l)
         mx, mean = errors(got, want, valid_rows_mask(items, cfg.N, cfg.block_l, cfg.d))
@@ -263,7 +276,7 @@ def main():
     if not args.no_e2e:
         qh, kh, vh = (t.cpu().pin_memory() for t in (q, k, v))
         oh = torch.empty_like(qh).pin_memory()
-        da.distr_attn_fwd_host(qh, kh, vh, oh, block_l=cfg.block_l, group_size=G)  # warm
+        da.distr_attn_fwd_host(qh, kh, vh, oh, block_l=cfg.block_l, group_size=G, q_shard=qsh)  # warm
         n_e2e = max(1, min(args.steps, 3))
         barrier()
         t0 = time.perf_counter()
@@ -271,13 +284,14 @@ def main():
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         for _ in range(n_e2e):
-            da.distr_attn_fwd_host(qh, kh, vh, oh, block_l=cfg.block_l, group_size=G)
+            da.distr_attn_fwd_host(qh, kh, vh, oh, block_l=cfg.block_l, group_size=G, q_shard=qsh)
         e1.record(stream)
         barrier()
         e_ms = max_over_ranks([e0.elapsed_time(e1) / n_e2e], device=dev)[0]
         nbytes = q.numel() * q.element_size()
         e2e = {"value": e_ms, "unit": "ms", "h2d_bytes_per_step": 3 * nbytes * world,
                "d2h_bytes_per_step": nbytes * world, "steps": n_e2e,
+               "note": "q-sharded: every rank copies the whole batch in and out" if qsh else None,
                "api": "distr_attn_fwd_host (pinned host buffers)"}
         del qh, kh, vh, oh
 
@@ -298,8 +312,11 @@ def main():
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
             "config": {"workload": f"{cfg.name}: B={cfg.B} H={cfg.H} N={cfg.N} d={cfg.d} "
-                                   f"block_l={cfg.block_l} G*={G} bf16 non-causal",
-                       "B_per_rank": B, "parallelism": f"(b,h)-sharded x{world}",
+                                   f"block_l={cfg.block_l} G*={G} bf16 "
+                                   f"{'causal' if cfg.causal else 'non-causal'}",
+                       "B_per_rank": B,
+                       "parallelism": (f"Q-tile-pair-sharded x{world}" if args.shard == "q"
+                                       else f"(b,h)-sharded x{world}"),
                        "l2": "inputs (17 GB) larger than L2, no flush"},
             "exact_ms": ex_ms, "speedup_vs_exact": ex_ms / ms,
             "attn_kernel_ms": attn_ms, "prep_kernel_ms": prep_ms, "exact_kernel_ms": ex_attn_ms,
