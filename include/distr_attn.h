@@ -110,6 +110,19 @@ int exact_attn_fwd_ex(const void* q, const void* k, const void* v, void* out, co
 int distr_attn_global_fwd_ex(const void* q, const void* k, const void* v, void* out, const da_params* p,
                              void* cuda_stream);
 
+/* Backward pass of DistrAttention (reading R18: the grouping of each Q
+ * block is held constant, so dQ lands on the representative columns only and every member of a
+ * group receives its fused column's dK). Inputs: the forward's q, k, v, out and its natural-log
+ * LSE (da_params.lse of the forward call, [B, H, N] fp32), and dout = dL/dout; outputs dq
+ * [B,H,N,d], dk, dv [B,H_kv,N,d] (bf16, overwritten). Same params as the forward (block_l,
+ * group_size, seed select the grouping; causal, scale; group_size = 1 gives exact attention
+ * gradients). bf16 only. First version: the attention GEMMs run on cuBLAS over chunks of query
+ * rows (library-managed workspace, ~2^27 fp32 score entries + fp32 dK/dV accumulators); the
+ * grouping, Q̃ expansion, softmax/dscore and the dQ fold are this library's kernels. The call
+ * synchronises the stream before returning. */
+int distr_attn_bwd_ex(const void* q, const void* k, const void* v, const void* out, const void* dout,
+                      const float* lse, void* dq, void* dk, void* dv, const da_params* p, void* cuda_stream);
+
 /* Run only the LSH step of the prep kernel and export p->bucket_ids and/or p->perm (at least one
  * must be non-NULL). Bit-exact contract with the CPU oracle (fp32 fma chain, ascending rows). */
 int distr_attn_hash(const void* q, const da_params* p, void* cuda_stream);

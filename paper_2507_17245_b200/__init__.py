@@ -20,6 +20,7 @@ __all__ = [
     "distr_attn_fwd", "distr_attn_fwd_ex", "exact_attn_fwd_ex", "distr_attn_fwd_host",
     "distr_attn_hash", "distr_attn_projection", "distr_attn_workspace_size", "make_params",
     "DistrAttnError", "last_launch_count", "distr_attn_plan", "distr_attn_global_fwd_ex",
+    "distr_attn_bwd_ex",
 ]
 
 _DT = {torch.bfloat16: DA_BF16, torch.float32: DA_F32}
@@ -102,6 +103,25 @@ def distr_attn_global_fwd_ex(q, k, v, out=None, *, group_size=2, seed=0, causal=
     check(_native.lib().distr_attn_global_fwd_ex(_ptr(q), _ptr(k), _ptr(v), _ptr(out), ctypes.byref(p),
                                                  _stream(stream)))
     return out
+
+
+def distr_attn_bwd_ex(q, k, v, out, dout, lse, *, block_l=128, group_size=2, seed=0, causal=False,
+                      scale=0.0, stream=None):
+    """Backward of DistrAttention (grouping held constant, reading R18): returns (dq, dk, dv).
+    `out` and `lse` ([B, H, N] fp32, natural log) come from the forward call with the same
+    params; group_size=1 gives exact-attention gradients."""
+    _check_tensors(q, k, v, out, dout, lse)
+    if lse is None or lse.dtype != torch.float32 or tuple(lse.shape) != tuple(q.shape[:3]):
+        raise ValueError("lse must be fp32 [B, H, N]")
+    if dout.shape != q.shape or dout.dtype != q.dtype:
+        raise ValueError("dout must match q")
+    dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+    p = make_params(q, k, block_l=block_l, group_size=group_size, seed=seed, causal=causal,
+                    scale=scale, v=v, out=out)
+    check(_native.lib().distr_attn_bwd_ex(_ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(dout), _ptr(lse),
+                                          _ptr(dq), _ptr(dk), _ptr(dv), ctypes.byref(p),
+                                          _stream(stream)))
+    return dq, dk, dv
 
 
 def exact_attn_fwd_ex(q, k, v, out=None, *, block_l=128, causal=False, scale=0.0, lse=None,

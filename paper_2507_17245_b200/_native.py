@@ -21,7 +21,7 @@ EXPORTED = (
     "exact_attn_fwd_ex", "distr_attn_hash", "distr_attn_projection", "distr_attn_workspace_size",
     "distr_attn_status_string", "distr_attn_last_error", "distr_attn_last_launch_count",
     "distr_attn_set_profile_events", "distr_attn_set_trace", "distr_attn_plan",
-    "distr_attn_global_fwd_ex",
+    "distr_attn_global_fwd_ex", "distr_attn_bwd_ex",
 )
 
 
@@ -82,6 +82,7 @@ def lib() -> ctypes.CDLL:
             L.distr_attn_last_launch_count.restype = i32
             L.distr_attn_set_profile_events.argtypes = [vp, vp, vp]
             L.distr_attn_set_trace.argtypes = [vp]
+            L.distr_attn_bwd_ex.argtypes = [vp] * 9 + [P, vp]
             L.distr_attn_plan.argtypes = [i32, i32, i32, i32, i32, ctypes.POINTER(DaPlan)]
             _lib = L
     return _lib

@@ -20,7 +20,7 @@ CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libdistr_attn.so")
 BUILD = os.path.join(HERE, "_build")
-SOURCES = ["api.cu", "prep.cu", "prep_global.cu", "attn.cu"]
+SOURCES = ["api.cu", "prep.cu", "prep_global.cu", "bwd.cu", "attn.cu"]
 HEADERS = ["ptx.cuh", "internal.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -62,7 +62,7 @@ def build(force: bool = False, jobs: int = 4, verbose: bool = False) -> str:
                 sys.stderr.write(log)
     if force or _stale(LIB, objs):
         tmp = LIB + ".tmp"
-        cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs]
+        cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcublas"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")

@@ -17,6 +17,7 @@
 #include "../../include/distr_attn.h"
 #include "../../include/distr_attn_profile.h"
 #include "internal.h"
+#include <cublas_v2.h>
 
 namespace {
 
@@ -422,6 +423,81 @@ int forward_global(const void* q, const void* k, const void* v, void* out, const
   return DA_OK;
 }
 
+std::map<int, Pool> g_bwd_pool;  // per-device backward workspace
+std::map<int, cublasHandle_t> g_cublas;
+
+int get_cublas(int dev, cublasHandle_t* h) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  auto it = g_cublas.find(dev);
+  if (it == g_cublas.end()) {
+    cublasHandle_t hh;
+    if (cublasCreate(&hh) != CUBLAS_STATUS_SUCCESS) return fail(DA_ERR_CUDA, "cublasCreate failed");
+    it = g_cublas.emplace(dev, hh).first;
+  }
+  *h = it->second;
+  return DA_OK;
+}
+
+int backward(const void* q, const void* k, const void* v, const void* o, const void* dout, const float* lse,
+             void* dq, void* dk, void* dv, const da_params* p, cudaStream_t st) {
+  Plan P;
+  if (int s = validate(p, true, &P)) return s;
+  if (!q || !k || !v || !o || !dout || !lse || !dq || !dk || !dv) return fail(DA_ERR_INVALID, "null pointer");
+  if (P.f32) return fail(DA_ERR_PRECONDITION, "backward: bf16 tensors only");
+  int dev;
+  if (int s = current_device(&dev)) return s;
+  const size_t BH = (size_t)P.B * P.H, BHkv = (size_t)P.B * P.Hkv, N = P.N, d = P.d;
+  // chunking: R query rows x nb heads per batched GEMM, fp32 score tiles bounded to ~2^27 entries
+  const int R = (int)std::min<size_t>(N, 1024);
+  const int nb = (int)std::max<size_t>(1, std::min<size_t>(BH, ((size_t)1 << 27) / ((size_t)R * N)));
+  const size_t n_it = ((BH + nb - 1) / nb) * ((N + R - 1) / R);
+  size_t o_ = 0;
+  auto take = [&](size_t bytes) { size_t at = o_; o_ = al256(o_ + bytes); return at; };
+  const size_t off_perm = take(BH * P.nqb * d), off_qt = take(BH * N * d * 2), off_D = take(BH * N * 4);
+  const size_t tile = (size_t)nb * R * N;
+  const size_t off_S = take(tile * 4), off_dP = take(tile * 4), off_P16 = take(tile * 2), off_dS = take(tile * 2);
+  const size_t off_dqt = take((size_t)nb * R * d * 4), off_dk = take(BH * N * d * 4), off_dv = take(BH * N * d * 4);
+  const size_t off_ptr = take(n_it * 11 * nb * sizeof(void*));
+  void* w;
+  if (int s = get_pool(g_bwd_pool, dev, o_, &w)) return s;
+  uint8_t* ws = static_cast<uint8_t*>(w);
+  const float* proj = nullptr;
+  if (int s = get_projection(dev, p->seed, P.l, st, &proj)) return s;
+  cublasHandle_t h;
+  if (int s = get_cublas(dev, &h)) return s;
+  // the grouping of every Q block (held constant, R18): the same hash as the forward
+  da::PrepArgs pa{};
+  pa.q = q; pa.k = k; pa.in_f32 = 0;
+  pa.BH = (int)BH; pa.BHkv = (int)BHkv; pa.N = P.N; pa.d = P.d; pa.block_l = P.l; pa.G = P.G; pa.HB = P.HB;
+  pa.DR = P.DR; pa.nqb = P.nqb; pa.N_pad = P.N_pad; pa.proj = proj;
+  pa.perm_ws = ws + off_perm;
+  pa.n_hash_ctas = (int)(BH * P.nqb);
+  DA_CUDA(da::launch_prep(pa, st));
+  da::BwdArgs a{};
+  a.q = static_cast<const uint16_t*>(q); a.k = static_cast<const uint16_t*>(k);
+  a.v = static_cast<const uint16_t*>(v); a.o = static_cast<const uint16_t*>(o);
+  a.dout = static_cast<const uint16_t*>(dout); a.lse = lse; a.perm = ws + off_perm;
+  a.dq = static_cast<uint16_t*>(dq); a.dk = static_cast<uint16_t*>(dk); a.dv = static_cast<uint16_t*>(dv);
+  a.BH = (int)BH; a.BHkv = (int)BHkv; a.H = P.H; a.Hkv = P.Hkv; a.N = P.N; a.d = P.d; a.G = P.G;
+  a.nqb = P.nqb; a.block_l = P.l; a.causal = P.causal; a.scale = P.scale;
+  a.R = R; a.nb = nb;
+  a.qt = reinterpret_cast<uint16_t*>(ws + off_qt); a.D = reinterpret_cast<float*>(ws + off_D);
+  a.S = reinterpret_cast<float*>(ws + off_S); a.dP = reinterpret_cast<float*>(ws + off_dP);
+  a.P16 = reinterpret_cast<uint16_t*>(ws + off_P16); a.dS16 = reinterpret_cast<uint16_t*>(ws + off_dS);
+  a.dqt = reinterpret_cast<float*>(ws + off_dqt);
+  a.dk_acc = reinterpret_cast<float*>(ws + off_dk); a.dv_acc = reinterpret_cast<float*>(ws + off_dv);
+  std::vector<const void*> host(n_it * 11 * nb);
+  a.host_ptrs = host.data();
+  a.dev_ptrs = reinterpret_cast<void**>(ws + off_ptr);
+  int rc = da::run_backward(a, h, st);
+  if (rc >= 1000) return fail(DA_ERR_CUDA, "cuBLAS error %d in backward", rc - 1000);
+  if (rc) return fail(DA_ERR_CUDA, "CUDA error in backward: %s", cudaGetErrorString((cudaError_t)rc));
+  // the pageable pointer table must outlive the async upload
+  DA_CUDA(cudaStreamSynchronize(st));
+  g_last_launches = -1;  // kernels + cuBLAS calls (not counted)
+  return DA_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -453,6 +529,11 @@ int distr_attn_fwd_ex(const void* q, const void* k, const void* v, void* out, co
 int exact_attn_fwd_ex(const void* q, const void* k, const void* v, void* out, const da_params* p,
                       void* cuda_stream) {
   return forward(q, k, v, out, p, static_cast<cudaStream_t>(cuda_stream), false);
+}
+
+int distr_attn_bwd_ex(const void* q, const void* k, const void* v, const void* out, const void* dout,
+                      const float* lse, void* dq, void* dk, void* dv, const da_params* p, void* cuda_stream) {
+  return backward(q, k, v, out, dout, lse, dq, dk, dv, p, static_cast<cudaStream_t>(cuda_stream));
 }
 
 int distr_attn_global_fwd_ex(const void* q, const void* k, const void* v, void* out, const da_params* p,

@@ -58,6 +58,26 @@ struct GlobalArgs {
   uint16_t* khat;        // [BH][N][d/G]
 };
 cudaError_t launch_global_prep(const GlobalArgs& a, cudaStream_t st);
+
+// Backward (bwd.cu). bf16 tensors [B*H or B*H_kv][N][d]; everything else workspace.
+struct BwdArgs {
+  const uint16_t *q, *k, *v, *o, *dout;
+  const float* lse;       // [BH][N] natural-log sum-exp from the forward
+  const uint8_t* perm;    // [BH][nqb][d] (hash of q)
+  uint16_t *dq, *dk, *dv;  // outputs
+  int BH, BHkv, H, Hkv, N, d, G, nqb, block_l, causal;
+  float scale;
+  int R, nb;              // query rows per chunk, heads per batched GEMM
+  uint16_t* qt;           // [BH][N][d] Q̃
+  float* D;               // [BH][N]
+  float *S, *dP;          // [nb][R][N] fp32
+  uint16_t *P16, *dS16;   // [nb][R][N] bf16
+  float* dqt;             // [nb][R][d]
+  float *dk_acc, *dv_acc; // [BH][N][d] fp32
+  const void** host_ptrs; // host staging for the batched-GEMM pointer arrays
+  void** dev_ptrs;        // device copy
+};
+int run_backward(const BwdArgs& a, void* cublas_handle, cudaStream_t st);  // 0 = ok
 cudaError_t launch_convert_bf16(const float* src, uint16_t* dst, size_t n, cudaStream_t st);
 
 // Which kernel flavour: DISTR with (d, G, HB) or exact with d.

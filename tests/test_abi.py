@@ -31,7 +31,7 @@ def header_functions():
 
 def test_exports_every_declared_symbol(L):
     names = header_functions()
-    assert len(names) == 15, names
+    assert len(names) == 16, names
     assert names == set(_native.EXPORTED)
     for n in names:
         assert hasattr(L, n), n
