@@ -1,0 +1,47 @@
+"""Backward timing (distr_attn_bwd_ex): CUDA events around the C call, after
+warm-up, on the C4 shape (B=1 H=16 d=128) at N in {4k, 16k}, G* in {1, 2}.
+
+    python tools/bench_bwd.py > gpurun_out/bwd.json
+
+Executed FLOP per call: five GEMMs of 2·N·N_k·d (Ŝ = Q̃Kᵀ, dP = dO Vᵀ, dV = Pᵀ dO, dQ̃ = dŜ K,
+dK = dŜᵀ Q̃) per head; roofline against MEASURED_PEAKS bf16 (the GEMMs run on cuBLAS). The HBM
+traffic of the materialised score tiles (S, dP fp32; P, dŜ bf16: 12 B per (query, key) pair,
+written and read back) is reported beside it — this first version is bound by it, not by the MMAs.
+"""
+import json, os, sys
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import torch
+import paper_2507_17245_b200 as da
+from synth import CONFIGS, make_qkv
+
+peaks = {}
+try:
+    peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+except Exception:
+    pass
+peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 2250.0))
+for N in (4096, 16384):
+    for G in (1, 2):
+        c = CONFIGS["C4"].with_(B=1, H=16, H_kv=16, N=N, group_size=G)
+        q, k, v = make_qkv(c, device="cuda")
+        dout = torch.randn_like(q.float()).bfloat16()
+        lse = torch.empty(q.shape[:3], dtype=torch.float32, device="cuda")
+        out = da.distr_attn_fwd_ex(q, k, v, group_size=G, lse=lse)
+        for _ in range(2):
+            da.distr_attn_bwd_ex(q, k, v, out, dout, lse, group_size=G)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        steps = 5
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(steps):
+            da.distr_attn_bwd_ex(q, k, v, out, dout, lse, group_size=G)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / steps
+        flop = 5 * 2.0 * N * N * c.d * c.H
+        rec = {"N": N, "G": G, "B": 1, "H": 16, "d": 128, "bwd_ms": ms,
+               "tflops_executed": flop / (ms * 1e-3) / 1e12, "peak_tflops": peak,
+               "frac_of_peak": flop / (ms * 1e-3) / 1e12 / peak,
+               "score_tile_bytes": 12.0 * N * N * c.H * 2}
+        print(json.dumps(rec), flush=True)
