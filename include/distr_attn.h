@@ -24,7 +24,7 @@
  *   - Thread safety: the projection cache and workspace pool are mutex-protected; concurrent
  *     calls that share a library-managed workspace on one device must use one stream.
  *
- * Supported envelope: d in {64, 128}; block_l in {64, 128}; G* (group_size) in {1, 2, 4, 8} with
+ * Supported envelope: d in {32, 64, 128}; block_l in {64, 128}; G* (group_size) in {1, 2, 4, 8} with
  * d % G* == 0 and the reduced width (128 / block_l) * d / G* in [16, 128]; any N >= 1 (ragged
  * tails handled); any B, H >= 1 with B*H, B*H_kv < 65536.
  */

@@ -138,7 +138,8 @@ int validate(const da_params* p, bool distr, Plan* P) {
   if (p->causal != 0 && p->causal != 1) return fail(DA_ERR_INVALID, "causal must be 0/1");
   if ((long long)p->B * p->H >= 65536 || (long long)p->B * p->H_kv >= 65536)
     return fail(DA_ERR_INVALID, "B*H too large");
-  if (p->d != 64 && p->d != 128) return fail(DA_ERR_PRECONDITION, "d=%d unsupported (64|128)", p->d);
+  if (p->d != 32 && p->d != 64 && p->d != 128)
+    return fail(DA_ERR_PRECONDITION, "d=%d unsupported (32|64|128)", p->d);
   if (p->block_l != 64 && p->block_l != 128)
     return fail(DA_ERR_PRECONDITION, "block_l=%d unsupported (64|128)", p->block_l);
   const int G = distr ? p->group_size : 1;
@@ -321,13 +322,14 @@ int forward(const void* q, const void* k, const void* v, void* out, const da_par
   }
 
   CUtensorMap tmA, tmK, tmV;
-  if (int s = make_map(&tmA, a_src, P.d, P.N, BH, 64, 128, 128)) return s;  // natural Q tiles
+  const uint32_t rb = P.d >= 64 ? 64 : (uint32_t)P.d;  // natural-row box: 64 columns (32 for d = 32)
+  if (int s = make_map(&tmA, a_src, P.d, P.N, BH, rb, 128, (int)rb * 2)) return s;  // natural Q tiles
   if (distr) {
     if (int s = make_map(&tmK, k_src, P.N_pad, P.d, BHkv, 128, P.d, 0)) return s;
   } else {
-    if (int s = make_map(&tmK, k_src, P.d, P.N, BHkv, 64, 128, 128)) return s;
+    if (int s = make_map(&tmK, k_src, P.d, P.N, BHkv, rb, 128, (int)rb * 2)) return s;
   }
-  if (int s = make_map(&tmV, kv_v, P.d, P.N, BHkv, 64, 128, 128)) return s;
+  if (int s = make_map(&tmV, kv_v, P.d, P.N, BHkv, rb, 128, (int)rb * 2)) return s;
 
   da::AttnArgs aa{};
   aa.N = P.N; aa.H = P.H; aa.H_kv = P.Hkv; aa.nqt = P.nqt; aa.nkt = P.nkt; aa.nqb = P.nqb; aa.block_l = P.l;
@@ -403,7 +405,8 @@ int forward_global(const void* q, const void* k, const void* v, void* out, const
   CUtensorMap tmA, tmK, tmV;
   if (int s = make_map(&tmA, g.qhat, DR, P.N, BH, sw / 2, 128, sw)) return s;
   if (int s = make_map(&tmK, g.khat, DR, P.N, BH, sw / 2, 128, sw)) return s;
-  if (int s = make_map(&tmV, v, P.d, P.N, BHkv, 64, 128, 128)) return s;
+  const uint32_t rb = P.d >= 64 ? 64 : (uint32_t)P.d;
+  if (int s = make_map(&tmV, v, P.d, P.N, BHkv, rb, 128, (int)rb * 2)) return s;
   da::AttnArgs aa{};
   aa.N = P.N; aa.H = P.H; aa.H_kv = P.Hkv; aa.nqt = P.nqt; aa.nkt = P.nkt; aa.nqb = P.nqb; aa.block_l = P.l;
   aa.pair_offset = P.pair_off; aa.pair_stride = P.pair_stride;

@@ -71,6 +71,10 @@ struct Cfg {
   // distr: the natural Q tiles (K-major SW128 boxes, 128 rows x d) are staged for the in-CTA
   // hash / Q̂ build in the V ring, or in the K+V rings when the V ring alone is too small.
   static constexpr int QT_BYTES = BM * D * 2;
+  // natural Q / V tiles in smem: boxes of RB columns (64, or 32 for d = 32), RB*2-byte rows,
+  // swizzled SWIZZLE_{RB*2}B
+  static constexpr int RB = D >= 64 ? 64 : D;
+  static constexpr int RB_SWB = RB == 64 ? 3 : 2;
   static constexpr bool STAGE_IN_V = NS * V_BYTES >= 2 * QT_BYTES;
   static_assert(DR % 16 == 0 && DR >= 16 && DR <= 128, "reduced width");
   static_assert(A_COLS % A_BOX_COLS == 0, "A boxes");
@@ -124,9 +128,10 @@ DA_DEV void qhat_prologue(const AttnArgs& args, uint64_t* bars, const uint8_t* s
   float* proj_t = reinterpret_cast<float*>(scratch);           // [l][16]
   uint32_t* key_s = reinterpret_cast<uint32_t*>(scratch + 8192);  // [2][HB][D] keys + [2][HB][D][2] u8 parts
   auto wsync = [] { asm volatile("bar.sync 5, 384;" ::: "memory"); };
-  auto q_at = [&](int t, int r, int c) -> uint32_t {  // bf16 bits of staged Q(t, r, c)
-    const uint32_t off = (uint32_t)(t * C::QT_BYTES + (c >> 6) * (BM * 128) + r * 128 + (c & 63) * 2);
-    return *reinterpret_cast<const uint16_t*>(sQ + swz(off, 3));
+  // byte offset of staged Q(t, r, c): box c / RB, RB*2-byte rows, SWIZZLE_{RB*2}B
+  auto q_off = [&](int t, int r, int c) -> uint32_t {
+    return (uint32_t)(t * C::QT_BYTES + (c / C::RB) * (BM * C::RB * 2)) +
+           swz((uint32_t)(r * C::RB * 2 + (c % C::RB) * 2), C::RB_SWB);
   };
   const bool hash = args.perm == nullptr;
   if (hash)
@@ -144,16 +149,13 @@ DA_DEV void qhat_prologue(const AttnArgs& args, uint64_t* bars, const uint8_t* s
       const int t = cp / (HB * D / 2), hb = (cp / (D / 2)) % HB, c = (cp % (D / 2)) * 2;
       const int row0 = (qt0 + t) * BM + hb * L;  // first global row of this hash block
       const int rows = max(0, min(L, args.N - row0));
-      // staged Q(t, hb*L + r, c): box c/64, row stride 128 B, 16-B chunk ((c%64)/8) ^ (row%8)
-      const uint8_t* qcol = sQ + t * C::QT_BYTES + (c >> 6) * (BM * 128) + hb * L * 128 + (c & 7) * 2;
-      const uint32_t chunk = (uint32_t)((c & 63) >> 3);
       float2 ya[4], yb[4];  // column c / c+1, projection rows 8kh .. 8kh+7
 #pragma unroll
       for (int m = 0; m < 4; ++m) ya[m] = yb[m] = make_float2(0.0f, 0.0f);
       const float* pr = proj_t + 8 * kh;
 #pragma unroll 2
       for (int r = 0; r < rows; ++r) {
-        const uint32_t q2 = *reinterpret_cast<const uint32_t*>(qcol + r * 128 + ((chunk ^ (uint32_t)(r & 7)) << 4));
+        const uint32_t q2 = *reinterpret_cast<const uint32_t*>(sQ + q_off(t, hb * L + r, c));
         const float qa = __uint_as_float(q2 << 16), qb = __uint_as_float(q2 & 0xFFFF0000u);
         const float4 p0 = *reinterpret_cast<const float4*>(pr + r * 16);
         const float4 p1 = *reinterpret_cast<const float4*>(pr + r * 16 + 4);
@@ -237,10 +239,7 @@ DA_DEV void qhat_prologue(const AttnArgs& args, uint64_t* bars, const uint8_t* s
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         const int c = src[hbr][e];
-        v[e] = c < 0 ? 0u
-                     : *reinterpret_cast<const uint16_t*>(
-                           sQ + t * C::QT_BYTES + (c >> 6) * (BM * 128) + r * 128 +
-                           ((((uint32_t)(c & 63) >> 3) ^ (uint32_t)(r & 7)) << 4) + (c & 7) * 2);
+        v[e] = c < 0 ? 0u : *reinterpret_cast<const uint16_t*>(sQ + q_off(t, r, c));
       }
       *reinterpret_cast<uint4*>(sA + t * C::A_BYTES + swz(dcol + r * C::A_SW, C::A_SWB)) =
           make_uint4(v[0] | (v[1] << 16), v[2] | (v[3] << 16), v[4] | (v[5] << 16), v[6] | (v[7] << 16));
@@ -325,8 +324,9 @@ __global__ void __launch_bounds__(threads_of<DISTR>(), 1)
       uint8_t* sQ0 = C::STAGE_IN_V ? sV : sK;
       mbar_arrive_expect_tx(&bars[B_Q], ntile * C::QT_BYTES);
       for (int t = 0; t < ntile; ++t)
-        for (int bx = 0; bx < D / 64; ++bx)
-          tma_load_3d(sQ0 + t * C::QT_BYTES + bx * (BM * 128), &tmA, &bars[B_Q], bx * 64, (qt0 + t) * BM, bh);
+        for (int bx = 0; bx < D / C::RB; ++bx)
+          tma_load_3d(sQ0 + t * C::QT_BYTES + bx * (BM * C::RB * 2), &tmA, &bars[B_Q], bx * C::RB, (qt0 + t) * BM,
+                      bh);
     } else {
       mbar_arrive_expect_tx(&bars[B_Q], ntile * C::A_BYTES);
       for (int t = 0; t < ntile; ++t)
@@ -389,8 +389,9 @@ __global__ void __launch_bounds__(threads_of<DISTR>(), 1)
         const uint32_t ph = (i / NS) & 1;
         mbar_wait(&bars[B_VEMPTY + s], ph ^ 1);
         mbar_arrive_expect_tx(&bars[B_VFULL + s], C::V_BYTES);
-        for (int bx = 0; bx < D / 64; ++bx)
-          tma_load_3d(sV + s * C::V_BYTES + bx * (BN * 128), &tmV, &bars[B_VFULL + s], bx * 64, i * BN, bhkv);
+        for (int bx = 0; bx < D / C::RB; ++bx)
+          tma_load_3d(sV + s * C::V_BYTES + bx * (BN * C::RB * 2), &tmV, &bars[B_VFULL + s], bx * C::RB, i * BN,
+                      bhkv);
       }
     }
   } else if (warp == 1) {
@@ -437,8 +438,9 @@ __global__ void __launch_bounds__(threads_of<DISTR>(), 1)
         const uint32_t p_tmem = tmem + kColS + 128u * t;
 #pragma unroll
         for (int kk = 0; kk < BN / 16; ++kk) {
-          // V as the MN-major B operand: 64-column blocks (LBO) of 8-key groups (SBO).
-          const uint64_t vdesc = make_sdesc(v_base + kk * 2048, BN * 128, 1024, kSw128);
+          // V as the MN-major B operand: RB-column blocks (LBO) of 8-key groups (SBO).
+          const uint64_t vdesc = make_sdesc(v_base + kk * 16 * C::RB * 2, BN * C::RB * 2, 8 * C::RB * 2,
+                                            C::RB == 64 ? kSw128 : kSw64);
           mma_ts(tmem + (uint32_t)(t * D), p_tmem + kk * 8, vdesc, IDESC_PV, (j > 0 || kk > 0) ? 1u : 0u);
         }
         if (j == nkt_t[t] - 1) mma_commit(&bars[B_OFULL + t]);
@@ -481,6 +483,7 @@ __global__ void __launch_bounds__(threads_of<DISTR>(), 1)
     // While these warps run tile t's exp phase the tensor core computes the other tile.
     const int half = (warp - 4) >> 2;
     const int quad = warp & 3;
+    constexpr int OC = D / 2 >= 32 ? 32 : 16;  // O columns per TMEM load in the rescale / epilogue
     const int row = quad * 32 + lane;
     const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
     float* xmax = reinterpret_cast<float*>(bars + B_COUNT);  // max [2 parity][2 t][2 half][128], sums [2 t][2 half][128]
@@ -538,13 +541,13 @@ __global__ void __launch_bounds__(threads_of<DISTR>(), 1)
           if (__any_sync(0xffffffffu, need)) {
             const float f = need ? ex2(m[t] - mnew) : 1.0f;
 #pragma unroll
-            for (int c = 0; c < D / 64; ++c) {
-              uint32_t r[32];
-              tmem_ld32(tO + 32u * c, r);
+            for (int c = 0; c < D / 2 / OC; ++c) {
+              uint32_t r[OC];
+              tmem_ldn<OC>(tO + (uint32_t)(OC * c), r);
               tmem_ld_wait();
 #pragma unroll
-              for (int e = 0; e < 32; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * f);
-              tmem_st32(tO + 32u * c, r);
+              for (int e = 0; e < OC; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * f);
+              tmem_stn<OC>(tO + (uint32_t)(OC * c), r);
             }
             if (need) {
               l[t] *= f;
@@ -594,22 +597,22 @@ __global__ void __launch_bounds__(threads_of<DISTR>(), 1)
       tc_fence_after();
       const float inv = 1.0f / lt;
 #pragma unroll
-      for (int c = 0; c < D / 64; ++c) {
-        uint32_t r[32];
-        tmem_ld32(tO + 32u * c, r);
+      for (int c = 0; c < D / 2 / OC; ++c) {
+        uint32_t r[OC];
+        tmem_ldn<OC>(tO + (uint32_t)(OC * c), r);
         tmem_ld_wait();
         if (q_row < args.N) {
-          const size_t off = ((size_t)bh * args.N + q_row) * D + half * (D / 2) + 32 * c;
+          const size_t off = ((size_t)bh * args.N + q_row) * D + half * (D / 2) + OC * c;
           if (args.out_f32) {
             float4* o = reinterpret_cast<float4*>(static_cast<float*>(args.out) + off);
 #pragma unroll
-            for (int e = 0; e < 8; ++e)
+            for (int e = 0; e < OC / 4; ++e)
               o[e] = make_float4(__uint_as_float(r[4 * e]) * inv, __uint_as_float(r[4 * e + 1]) * inv,
                                  __uint_as_float(r[4 * e + 2]) * inv, __uint_as_float(r[4 * e + 3]) * inv);
           } else {
             uint4* o = reinterpret_cast<uint4*>(static_cast<uint16_t*>(args.out) + off);
 #pragma unroll
-            for (int e = 0; e < 4; ++e)
+            for (int e = 0; e < OC / 8; ++e)
               o[e] = make_uint4(pack_bf16x2(__uint_as_float(r[8 * e]) * inv, __uint_as_float(r[8 * e + 1]) * inv),
                                 pack_bf16x2(__uint_as_float(r[8 * e + 2]) * inv, __uint_as_float(r[8 * e + 3]) * inv),
                                 pack_bf16x2(__uint_as_float(r[8 * e + 4]) * inv, __uint_as_float(r[8 * e + 5]) * inv),
@@ -735,6 +738,8 @@ constexpr size_t smem_of() {
 
 #define DA_DISPATCH(MACRO)                                                          \
   if (!distr) {                                                                     \
+    if (d == 32 && G == 1) MACRO(32, false, 1, 1);                                  \
+    if (d == 32 && G == 2) MACRO(32, false, 2, 1);                                  \
     if (d == 64 && G == 1) MACRO(64, false, 1, 1);                                  \
     if (d == 64 && G == 2) MACRO(64, false, 2, 1);                                  \
     if (d == 64 && G == 4) MACRO(64, false, 4, 1);                                  \
@@ -743,6 +748,10 @@ constexpr size_t smem_of() {
     if (d == 128 && G == 4) MACRO(128, false, 4, 1);                                \
     if (d == 128 && G == 8) MACRO(128, false, 8, 1);                                \
   } else {                                                                          \
+    if (d == 32 && G == 1 && HB == 1) MACRO(32, true, 1, 1);                        \
+    if (d == 32 && G == 1 && HB == 2) MACRO(32, true, 1, 2);                        \
+    if (d == 32 && G == 2 && HB == 1) MACRO(32, true, 2, 1);                        \
+    if (d == 32 && G == 2 && HB == 2) MACRO(32, true, 2, 2);                        \
     if (d == 64 && G == 1 && HB == 1) MACRO(64, true, 1, 1);                        \
     if (d == 64 && G == 1 && HB == 2) MACRO(64, true, 1, 2);                        \
     if (d == 64 && G == 2 && HB == 1) MACRO(64, true, 2, 1);                        \

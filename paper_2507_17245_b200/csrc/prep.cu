@@ -67,8 +67,8 @@ DA_DEV void hash_cta(const PrepArgs& a, int it, uint8_t* smem) {
   const int lsh = ilog2(a.block_l);
   T* q_s = reinterpret_cast<T*>(smem);                                 // [rows][QP]
   float* proj_t = reinterpret_cast<float*>(smem + QBYTES);             // [r][16]
-  uint32_t* pat_s = reinterpret_cast<uint32_t*>(proj_t + kMaxL * 16);  // [NKG][D]
-  uint32_t* key_s = pat_s + 4 * D;                                     // [D]
+  uint32_t* pat_s = reinterpret_cast<uint32_t*>(proj_t + kMaxL * 16);  // [NKG][D] = kThreads
+  uint32_t* key_s = pat_s + kThreads;                                  // [D]
   uint8_t* perm_s = reinterpret_cast<uint8_t*>(key_s + D);             // [D]
 
   // Stage the Q block (16-byte global loads, coalesced) and the transposed projection [r][16].
@@ -97,8 +97,8 @@ DA_DEV void hash_cta(const PrepArgs& a, int it, uint8_t* smem) {
   __syncthreads();
 
   // Projection: thread -> (column c, group of KPT consecutive projection rows).
-  constexpr int NKG = kThreads / D;  // 2 (d=128) or 4 (d=64)
-  constexpr int KPT = 16 / NKG;      // 8 or 4
+  constexpr int NKG = kThreads / D;  // 2 (d=128), 4 (d=64) or 8 (d=32)
+  constexpr int KPT = 16 / NKG;      // 8, 4 or 2
   const int c = threadIdx.x % D, kg = threadIdx.x / D;
   const int k0 = kg * KPT;
   float2 y[KPT / 2];
@@ -107,11 +107,16 @@ DA_DEV void hash_cta(const PrepArgs& a, int it, uint8_t* smem) {
   for (int r = 0; r < rows; ++r) {
     const float qv = load_f<T>(q_s + r * QP + c);
     const float2 qq = make_float2(qv, qv);
+    if constexpr (KPT == 2) {
+      const float2 pa = *reinterpret_cast<const float2*>(proj_t + r * 16 + k0);
+      y[0] = fma2(pa, qq, y[0]);
+    } else {
 #pragma unroll
-    for (int m = 0; m < KPT / 4; ++m) {
-      const float4 pa = *reinterpret_cast<const float4*>(proj_t + r * 16 + k0 + 4 * m);
-      y[2 * m] = fma2(make_float2(pa.x, pa.y), qq, y[2 * m]);
-      y[2 * m + 1] = fma2(make_float2(pa.z, pa.w), qq, y[2 * m + 1]);
+      for (int m = 0; m < KPT / 4; ++m) {
+        const float4 pa = *reinterpret_cast<const float4*>(proj_t + r * 16 + k0 + 4 * m);
+        y[2 * m] = fma2(make_float2(pa.x, pa.y), qq, y[2 * m]);
+        y[2 * m + 1] = fma2(make_float2(pa.z, pa.w), qq, y[2 * m + 1]);
+      }
     }
   }
   uint32_t part = 0;
@@ -206,7 +211,7 @@ DA_DEV void kt_cta(const PrepArgs& a, int it, uint8_t* smem) {
   for (int u = 0; u < NIT; ++u) {
     const int i = threadIdx.x + u * kThreads;
     const int t = i / CPR, c8 = i % CPR;
-    const int f = (t & 7) ^ (((t >> 3) & 3) << 1);
+    const int f = ((t & 7) ^ (((t >> 3) & 3) << 1)) & (CPR - 1);  // d = 32: 4 chunks per key
     tile[t * CPR + (c8 ^ f)] = w[u];
   }
   __syncthreads();
@@ -223,7 +228,7 @@ DA_DEV void kt_cta(const PrepArgs& a, int it, uint8_t* smem) {
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const int ta = t + 2 * e, tb = ta + 1;
-      const int fa = (ta & 7) ^ (((ta >> 3) & 3) << 1), fb = (tb & 7) ^ (((tb >> 3) & 3) << 1);
+      const int fa = ((ta & 7) ^ (((ta >> 3) & 3) << 1)) & (CPR - 1), fb = ((tb & 7) ^ (((tb >> 3) & 3) << 1)) & (CPR - 1);
       const uint32_t lo = te[(ta * CPR + ((c >> 3) ^ fa)) * 8 + (c & 7)];
       const uint32_t hi = te[(tb * CPR + ((c >> 3) ^ fb)) * 8 + (c & 7)];
       w[e] = lo | (hi << 16);
@@ -250,7 +255,7 @@ __global__ void convert_kernel(const float* __restrict__ src, uint16_t* __restri
 template <typename T, int D>
 size_t prep_smem_bytes() {
   const size_t q = (size_t)kMaxL * q_pitch<T, D>() * sizeof(T);
-  const size_t hash = q + kMaxL * 16 * 4 + 4 * D * 4 + D * 4 + D + 16;
+  const size_t hash = q + kMaxL * 16 * 4 + kThreads * 4 + D * 4 + D + 16;
   const size_t kt = 64 * D * 2;
   return std::max(hash, kt);
 }
@@ -269,8 +274,11 @@ cudaError_t launch_prep_t(const PrepArgs& a, cudaStream_t st) {
 
 cudaError_t launch_prep(const PrepArgs& a, cudaStream_t st) {
   if (a.n_hash_ctas + a.n_kt_ctas == 0) return cudaSuccess;
-  if (a.in_f32) return a.d == 64 ? launch_prep_t<float, 64>(a, st) : launch_prep_t<float, 128>(a, st);
-  return a.d == 64 ? launch_prep_t<uint16_t, 64>(a, st) : launch_prep_t<uint16_t, 128>(a, st);
+  if (a.in_f32)
+    return a.d == 32 ? launch_prep_t<float, 32>(a, st)
+                     : a.d == 64 ? launch_prep_t<float, 64>(a, st) : launch_prep_t<float, 128>(a, st);
+  return a.d == 32 ? launch_prep_t<uint16_t, 32>(a, st)
+                   : a.d == 64 ? launch_prep_t<uint16_t, 64>(a, st) : launch_prep_t<uint16_t, 128>(a, st);
 }
 
 cudaError_t launch_convert_bf16(const float* src, uint16_t* dst, size_t n, cudaStream_t st) {

@@ -43,14 +43,14 @@ __global__ void __launch_bounds__(kT) global_hash_kernel(const GlobalArgs a) {
   constexpr int NIT = kChunk * VPR / kT;  // vectors per thread per chunk
   __shared__ __align__(16) uint16_t q_s[kChunk * QP];
   __shared__ __align__(16) float proj_t[kChunk * 16];  // [r][16]
-  __shared__ uint32_t pat_s[4 * D];
+  __shared__ uint32_t pat_s[kT];  // [NKG][D]
   __shared__ uint32_t key_s[D];
   __shared__ uint8_t perm_s[D];
   const int bh = blockIdx.x;
   const uint16_t* qg = a.q + (size_t)bh * a.N * D;
   const int nchunk = (a.N + kChunk - 1) / kChunk;
 
-  constexpr int NKG = kT / D;  // projection-row groups: 2 (d=128) or 4 (d=64)
+  constexpr int NKG = kT / D;  // projection-row groups: 2 (d=128), 4 (d=64) or 8 (d=32)
   constexpr int KPT = 16 / NKG;
   const int c = threadIdx.x % D, kg = threadIdx.x / D, k0 = kg * KPT;
   float2 y[KPT / 2];
@@ -92,11 +92,15 @@ __global__ void __launch_bounds__(kT) global_hash_kernel(const GlobalArgs a) {
     for (int r = 0; r < rows; ++r) {
       const float qv = __uint_as_float(((uint32_t)q_s[r * QP + c]) << 16);
       const float2 qq = make_float2(qv, qv);
+      if constexpr (KPT == 2) {
+        y[0] = fma2(*reinterpret_cast<const float2*>(proj_t + r * 16 + k0), qq, y[0]);
+      } else {
 #pragma unroll
-      for (int m = 0; m < KPT / 4; ++m) {
-        const float4 pa = *reinterpret_cast<const float4*>(proj_t + r * 16 + k0 + 4 * m);
-        y[2 * m] = fma2(make_float2(pa.x, pa.y), qq, y[2 * m]);
-        y[2 * m + 1] = fma2(make_float2(pa.z, pa.w), qq, y[2 * m + 1]);
+        for (int m = 0; m < KPT / 4; ++m) {
+          const float4 pa = *reinterpret_cast<const float4*>(proj_t + r * 16 + k0 + 4 * m);
+          y[2 * m] = fma2(make_float2(pa.x, pa.y), qq, y[2 * m]);
+          y[2 * m + 1] = fma2(make_float2(pa.z, pa.w), qq, y[2 * m + 1]);
+        }
       }
     }
   }
@@ -189,7 +193,9 @@ __global__ void __launch_bounds__(kT) global_gather_kernel(const GlobalArgs a) {
 }  // namespace
 
 cudaError_t launch_global_prep(const GlobalArgs& a, cudaStream_t st) {
-  if (a.d == 64)
+  if (a.d == 32)
+    global_hash_kernel<32><<<a.BH, kT, 0, st>>>(a);
+  else if (a.d == 64)
     global_hash_kernel<64><<<a.BH, kT, 0, st>>>(a);
   else
     global_hash_kernel<128><<<a.BH, kT, 0, st>>>(a);
@@ -198,7 +204,7 @@ cudaError_t launch_global_prep(const GlobalArgs& a, cudaStream_t st) {
   const dim3 grid((a.N + 63) / 64, a.BH);
 #define DA_GATHER(D_, G_) \
   if (a.d == D_ && a.G == G_) global_gather_kernel<D_, G_><<<grid, kT, 0, st>>>(a);
-  DA_GATHER(64, 1) DA_GATHER(64, 2) DA_GATHER(64, 4)
+  DA_GATHER(32, 1) DA_GATHER(32, 2) DA_GATHER(64, 1) DA_GATHER(64, 2) DA_GATHER(64, 4)
   DA_GATHER(128, 1) DA_GATHER(128, 2) DA_GATHER(128, 4) DA_GATHER(128, 8)
 #undef DA_GATHER
   return cudaGetLastError();

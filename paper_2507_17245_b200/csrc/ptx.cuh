@@ -173,6 +173,14 @@ DA_DEV void tmem_st8(uint32_t taddr, const uint32_t* r) {
                "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
                : "memory");
 }
+template <int NC>
+DA_DEV void tmem_ldn(uint32_t taddr, uint32_t (&r)[NC]) {
+  if constexpr (NC == 32) tmem_ld32(taddr, r); else tmem_ld16(taddr, r);
+}
+template <int NC>
+DA_DEV void tmem_stn(uint32_t taddr, const uint32_t (&r)[NC]) {
+  if constexpr (NC == 32) tmem_st32(taddr, r); else tmem_st16(taddr, r);
+}
 DA_DEV void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 DA_DEV void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 

@@ -45,7 +45,8 @@ def run_global(c: Config, *, dist="normal", seed=3, q=None, k=None, v=None, orac
     return errors(got, want)
 
 
-@pytest.mark.parametrize("d,G", [(64, 1), (64, 2), (64, 4), (128, 1), (128, 2), (128, 4), (128, 8)])
+@pytest.mark.parametrize("d,G", [(32, 1), (32, 2), (64, 1), (64, 2), (64, 4), (128, 1), (128, 2), (128, 4),
+                                 (128, 8)])
 @pytest.mark.parametrize("causal", [False, True])
 def test_global_parity(d, G, causal):
     mx, mean = run_global(cfg(B=2, H=4, H_kv=2, N=333, d=d, group_size=G, causal=causal))

@@ -59,6 +59,7 @@ def test_hash_bit_exact_all_configs(name):
 @pytest.mark.parametrize("dist", ["uniform", "clustered"])
 def test_hash_stress_distributions(dist):
     check_hash(cfg_small(N=197, d=64, block_l=64, H=3), dist=dist)
+    check_hash(cfg_small(N=200, d=32, block_l=64, H=2), dist=dist)
     check_hash(cfg_small(N=300, d=128, block_l=128, H=2), dist=dist)
 
 
@@ -119,7 +120,8 @@ def test_exact_parity_configs(name):
 @pytest.mark.parametrize("d,block_l,G", [(64, 64, 1), (64, 64, 2), (64, 64, 4), (64, 128, 1),
                                          (64, 128, 2), (64, 128, 4), (128, 128, 1),
                                          (128, 128, 2), (128, 128, 4), (128, 64, 2),
-                                         (128, 64, 4), (128, 128, 8), (128, 64, 8)])
+                                         (128, 64, 4), (128, 128, 8), (128, 64, 8), (32, 128, 1),
+                                         (32, 128, 2), (32, 64, 1), (32, 64, 2)])
 @pytest.mark.parametrize("causal", [False, True])
 def test_distr_parity_envelope(d, block_l, G, causal):
     # several Q/K tiles plus ragged tails, GQA (H=4 over H_kv=2)

@@ -8,7 +8,7 @@ from paper_2507_17245_b200.build import build
 
 build()
 
-ENVELOPE = [(d, l, g) for d in (64, 128) for l in (64, 128) for g in (1, 2, 4, 8)
+ENVELOPE = [(d, l, g) for d in (32, 64, 128) for l in (64, 128) for g in (1, 2, 4, 8)
             if d % g == 0 and d // g >= 16 and (128 // l) * d // g <= 128]
 
 
@@ -61,6 +61,7 @@ def test_tmem_bound_on_m():
     # tiles * (d + m) <= 512: d=128 leaves m <= 128, d=64 leaves m <= 192
     assert da.distr_attn_plan(4096, 128)["m_max_tmem"] == 128
     assert da.distr_attn_plan(4096, 64)["m_max_tmem"] == 192
+    assert da.distr_attn_plan(4096, 32)["m_max_tmem"] == 224
 
 
 def test_ctas_cover_all_q_tiles():
