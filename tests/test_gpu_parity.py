@@ -209,3 +209,28 @@ def test_error_against_exact_is_reported_not_gated():
     e_or = np.abs(di - ex).mean()
     e_gpu = np.abs(got - ex).mean()
     assert abs(e_gpu - e_or) < 0.1 * e_or
+
+
+# ------------------------------------------------------------------------------ in-CTA hashing
+# Sequences with more than 8 key tiles hash their Q blocks inside the attention CTA
+# (qhat_prologue); shorter ones in the prep launch. These cases keep the in-CTA path covered.
+@pytest.mark.parametrize("d,block_l,G", [(32, 128, 2), (64, 64, 2), (64, 128, 4), (128, 128, 2),
+                                         (128, 64, 2), (128, 128, 8), (128, 128, 1)])
+@pytest.mark.parametrize("causal", [False, True])
+def test_in_cta_hash_path_parity(d, block_l, G, causal):
+    cfg = cfg_small(B=1, H=2, H_kv=1, N=1300, d=d, block_l=block_l, group_size=G, causal=causal)
+    q, k, v = make_qkv(cfg, device=DEV)
+    nqb = cfg.nqb
+    bk = torch.zeros((1, 2, nqb, d), dtype=torch.int16, device=DEV)
+    pm = torch.zeros((1, 2, nqb, d), dtype=torch.uint8, device=DEV)
+    out = da.distr_attn_fwd_ex(q, k, v, block_l=block_l, group_size=G, seed=13, causal=causal,
+                               bucket_ids=bk, perm=pm)
+    torch.cuda.synchronize()
+    ob, op = oracle.hash_all(to_np32(q), block_l, 13)
+    assert np.array_equal(bk.cpu().numpy().view(np.uint16), ob)
+    assert np.array_equal(pm.cpu().numpy(), op)
+    items = [(bh, qb) for bh in range(2) for qb in (0, 3, nqb - 1)]
+    want = oracle_items(q, k, v, items, block_l=block_l, G=G, seed=13, causal=causal)
+    got = gather_items(out, items, block_l)
+    mx, mean = errors(got, want, valid_rows_mask(items, cfg.N, block_l, d))
+    assert mx <= MAX_ABS and mean <= MEAN_ABS, (mx, mean)
