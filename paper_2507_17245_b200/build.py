@@ -20,7 +20,7 @@ CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libdistr_attn.so")
 BUILD = os.path.join(HERE, "_build")
-SOURCES = ["api.cu", "prep.cu", "prep_global.cu", "bwd.cu", "attn.cu"]
+SOURCES = ["api.cu", "prep.cu", "prep_global.cu", "bwd.cu", "bwd_fused.cu", "attn.cu"]
 HEADERS = ["ptx.cuh", "internal.h"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

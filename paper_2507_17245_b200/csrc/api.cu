@@ -441,6 +441,61 @@ int get_cublas(int dev, cublasHandle_t* h) {
   return DA_OK;
 }
 
+// Fused tcgen05 backward (bwd_fused.cu): hash -> Q̃ + D + padded lse -> dK/dV kernel -> dQ̃ kernel
+// -> fold. d in {64, 128}.
+int backward_fused(const void* q, const void* k, const void* v, const void* o, const void* dout, const float* lse,
+                   void* dq, void* dk, void* dv, const da_params* p, const Plan& P, cudaStream_t st) {
+  int dev;
+  if (int s = current_device(&dev)) return s;
+  const size_t BH = (size_t)P.B * P.H, BHkv = (size_t)P.B * P.Hkv, N = P.N, d = P.d;
+  const size_t N_pad = (N + 127) / 128 * 128;
+  size_t o_ = 0;
+  auto take = [&](size_t bytes) { size_t at = o_; o_ = al256(o_ + bytes); return at; };
+  const size_t off_perm = take(BH * P.nqb * d), off_qt = take(BH * N * d * 2), off_D = take(BH * N_pad * 4);
+  const size_t off_lse = take(BH * N_pad * 4), off_dqt = take(BH * N * d * 4);
+  void* w;
+  if (int s = get_pool(g_bwd_pool, dev, o_, &w)) return s;
+  uint8_t* ws = static_cast<uint8_t*>(w);
+  const float* proj = nullptr;
+  if (int s = get_projection(dev, p->seed, P.l, st, &proj)) return s;
+  da::PrepArgs pa{};
+  pa.q = q; pa.k = k; pa.in_f32 = 0;
+  pa.BH = (int)BH; pa.BHkv = (int)BHkv; pa.N = P.N; pa.d = P.d; pa.block_l = P.l; pa.G = P.G; pa.HB = P.HB;
+  pa.DR = P.DR; pa.nqb = P.nqb; pa.N_pad = P.N_pad; pa.proj = proj;
+  pa.perm_ws = ws + off_perm;
+  pa.n_hash_ctas = (int)(BH * P.nqb);
+  DA_CUDA(da::launch_prep(pa, st));
+  da::BwdArgs a{};
+  a.q = static_cast<const uint16_t*>(q); a.o = static_cast<const uint16_t*>(o);
+  a.dout = static_cast<const uint16_t*>(dout); a.perm = ws + off_perm;
+  a.BH = (int)BH; a.N = P.N; a.d = P.d; a.G = P.G; a.nqb = P.nqb; a.block_l = P.l;
+  a.qt = reinterpret_cast<uint16_t*>(ws + off_qt);
+  a.D = reinterpret_cast<float*>(ws + off_D);
+  a.Dstride = (int)N_pad;
+  float* lse_pad = reinterpret_cast<float*>(ws + off_lse);
+  DA_CUDA(da::launch_bwd_prologue(a, lse, lse_pad, (int)N_pad, st));
+  CUtensorMap tmQt, tmdO, tmK, tmV;
+  if (int s = make_map(&tmQt, a.qt, d, N, BH, 64, 128, 128)) return s;
+  if (int s = make_map(&tmdO, dout, d, N, BH, 64, 128, 128)) return s;
+  if (int s = make_map(&tmK, k, d, N, BHkv, 64, 128, 128)) return s;
+  if (int s = make_map(&tmV, v, d, N, BHkv, 64, 128, 128)) return s;
+  da::BwdFusedArgs f{};
+  f.tmQt = &tmQt; f.tmdO = &tmdO; f.tmK = &tmK; f.tmV = &tmV;
+  f.lse_pad = lse_pad; f.D_pad = a.D;
+  f.dqt = reinterpret_cast<float*>(ws + off_dqt);
+  f.dk = static_cast<uint16_t*>(dk); f.dv = static_cast<uint16_t*>(dv);
+  f.BH = (int)BH; f.BHkv = (int)BHkv; f.H = P.H; f.Hkv = P.Hkv; f.N = P.N; f.N_pad = (int)N_pad; f.d = P.d;
+  f.causal = P.causal; f.scale = P.scale;
+  record_ev(0, st);
+  DA_CUDA(da::launch_bwd_fused(f, st));
+  record_ev(1, st);
+  DA_CUDA(da::launch_fold_all(f.dqt, a.perm, static_cast<uint16_t*>(dq), (int)BH, P.N, P.d, P.G, P.nqb, P.l, st));
+  record_ev(2, st);
+  g_ev[0] = g_ev[1] = g_ev[2] = nullptr;
+  g_last_launches = 6;  // hash, Q̃/D, lse pad, dK/dV, dQ̃, fold
+  return DA_OK;
+}
+
 int backward(const void* q, const void* k, const void* v, const void* o, const void* dout, const float* lse,
              void* dq, void* dk, void* dv, const da_params* p, cudaStream_t st) {
   Plan P;
@@ -450,7 +505,8 @@ int backward(const void* q, const void* k, const void* v, const void* o, const v
   int dev;
   if (int s = current_device(&dev)) return s;
   const size_t BH = (size_t)P.B * P.H, BHkv = (size_t)P.B * P.Hkv, N = P.N, d = P.d;
-  // chunking: R query rows x nb heads per batched GEMM, fp32 score tiles bounded to ~2^27 entries
+  if (P.d != 32 && !getenv("DA_BWD_CUBLAS")) return backward_fused(q, k, v, o, dout, lse, dq, dk, dv, p, P, st);
+  // d = 32: cuBLAS GEMMs over chunks of R query rows x nb heads (fp32 score tiles <= 2^27 entries)
   const int R = (int)std::min<size_t>(N, 1024);
   const int nb = (int)std::max<size_t>(1, std::min<size_t>(BH, ((size_t)1 << 27) / ((size_t)R * N)));
   const size_t n_it = ((BH + nb - 1) / nb) * ((N + R - 1) / R);
@@ -484,7 +540,7 @@ int backward(const void* q, const void* k, const void* v, const void* o, const v
   a.BH = (int)BH; a.BHkv = (int)BHkv; a.H = P.H; a.Hkv = P.Hkv; a.N = P.N; a.d = P.d; a.G = P.G;
   a.nqb = P.nqb; a.block_l = P.l; a.causal = P.causal; a.scale = P.scale;
   a.R = R; a.nb = nb;
-  a.qt = reinterpret_cast<uint16_t*>(ws + off_qt); a.D = reinterpret_cast<float*>(ws + off_D);
+  a.qt = reinterpret_cast<uint16_t*>(ws + off_qt); a.D = reinterpret_cast<float*>(ws + off_D); a.Dstride = P.N;
   a.S = reinterpret_cast<float*>(ws + off_S); a.dP = reinterpret_cast<float*>(ws + off_dP);
   a.P16 = reinterpret_cast<uint16_t*>(ws + off_P16); a.dS16 = reinterpret_cast<uint16_t*>(ws + off_dS);
   a.dqt = reinterpret_cast<float*>(ws + off_dqt);

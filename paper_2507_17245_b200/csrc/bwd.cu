@@ -51,7 +51,7 @@ __global__ void qtilde_kernel(const BwdArgs a) {
     }
 #pragma unroll
     for (int s = 16; s > 0; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
-    if (lane == 0) a.D[row] = acc;
+    if (lane == 0) a.D[(size_t)bh * a.Dstride + r0 + r] = acc;
   }
 }
 
@@ -83,7 +83,7 @@ __global__ void dscore_kernel(const float* P, const float* dP, uint16_t* dS, con
     const int r = (int)(rr % R), b = (int)(rr / R);
     const size_t off = ((size_t)b * Rst + r) * ldn + col;
     const int qrow = r0 + r;
-    const float dv = qrow < N ? D[(size_t)(bh0 + b) * N + qrow] : 0.f;
+    const float dv = qrow < N ? D[(size_t)(bh0 + b) * N + qrow] : 0.f;  // cuBLAS path: Dstride = N
     dS[off] = f2bf(P[off] * (dP[off] - dv) * scale);
   }
 }
@@ -120,6 +120,30 @@ __global__ void reduce_kernel(const float* acc, uint16_t* dst, int BHkv, int rep
 
 int grid_for(size_t n) { return (int)std::min<size_t>((n + 255) / 256, 148 * 32); }
 
+__global__ void lse_pad_kernel(const float* lse, float* out, int BH, int N, int N_pad) {
+  const size_t total = (size_t)BH * N_pad;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+    const size_t bh = i / N_pad, r = i % N_pad;
+    out[i] = r < (size_t)N ? lse[bh * N + r] : __int_as_float(0x7f800000);  // +inf: P = 0 past N
+  }
+}
+
+// dQ[r][rep_j] = Σ_{c in G_j} dQ̃[r][c] over whole rows (fused path); non-representatives 0.
+__global__ void fold_all_kernel(const float* dqt, const uint8_t* perm, uint16_t* dq, int N, int d, int G, int nqb,
+                                int block_l) {
+  const int r = blockIdx.x, bh = blockIdx.y;
+  const uint8_t* pm = perm + ((size_t)bh * nqb + r / block_l) * d;
+  const float* src = dqt + ((size_t)bh * N + r) * d;
+  uint16_t* dst = dq + ((size_t)bh * N + r) * d;
+  for (int i = threadIdx.x; i < d; i += blockDim.x) dst[i] = 0;
+  __syncthreads();
+  for (int j = threadIdx.x; j < d / G; j += blockDim.x) {
+    float s = 0.f;
+    for (int g = 0; g < G; ++g) s += src[pm[j * G + g]];
+    dst[pm[j * G]] = f2bf(s);
+  }
+}
+
 #define CB(x)                                              \
   do {                                                     \
     cublasStatus_t s_ = (x);                               \
@@ -132,6 +156,20 @@ int grid_for(size_t n) { return (int)std::min<size_t>((n + 255) / 256, 148 * 32)
   } while (0)
 
 }  // namespace
+
+cudaError_t launch_bwd_prologue(const BwdArgs& a, const float* lse, float* lse_pad, int N_pad, cudaStream_t st) {
+  cudaError_t e = cudaMemsetAsync(a.D, 0, (size_t)a.BH * N_pad * 4, st);
+  if (e != cudaSuccess) return e;
+  qtilde_kernel<<<dim3((a.N + 63) / 64, a.BH), 256, 0, st>>>(a);
+  lse_pad_kernel<<<grid_for((size_t)a.BH * N_pad), 256, 0, st>>>(lse, lse_pad, a.BH, a.N, N_pad);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fold_all(const float* dqt, const uint8_t* perm, uint16_t* dq, int BH, int N, int d, int G,
+                            int nqb, int block_l, cudaStream_t st) {
+  fold_all_kernel<<<dim3(N, BH), 64, 0, st>>>(dqt, perm, dq, N, d, G, nqb, block_l);
+  return cudaGetLastError();
+}
 
 int run_backward(const BwdArgs& a, void* handle, cudaStream_t st) {
   cublasHandle_t h = static_cast<cublasHandle_t>(handle);

@@ -1,0 +1,394 @@
+// bwd_fused.cu — fused tcgen05 backward of DistrAttention (reading R18).
+//
+// With the grouping held constant, Ŝ = scale·Q̃Kᵀ (Q̃: every column replaced by its group
+// representative, per Q block — bwd.cu) and the backward is the attention backward on (Q̃, K, V)
+// followed by the dQ fold. Two kernels, no atomics, everything on the tensor cores:
+//
+//  bwd_kv_kernel — one CTA per (K/V tile of 128 keys, KV head); loops over the query heads of the
+//    GQA group and their Q tiles (causal: only tiles at or below the diagonal):
+//      Sᵀ  = K Q̃ᵀ    (SS, M = keys, N = queries, K = d)      -> TMEM [0, 128)
+//      dPᵀ = V dOᵀ   (SS)                                      -> TMEM [128, 256)
+//      8 warps: Pᵀ = exp2(Sᵀ·scale·log2e − lse·log2e), dŜᵀ = Pᵀ ∘ (dPᵀ − D)·scale -> bf16; warp
+//      half h (queries [64h, 64h+64)) writes into columns [64h, 64h+32) of the Sᵀ / dPᵀ ranges,
+//      its own (thread = key lane; lse, D of the tile's 128 queries arrive by bulk copy)
+//      dV += Pᵀ dO   (TS: A = Pᵀ from TMEM, B = dO MN-major)   -> TMEM [256, 256 + d)
+//      dK += dŜᵀ Q̃   (TS: A = dŜᵀ from TMEM, B = Q̃ MN-major)  -> TMEM [384, 384 + d)
+//    dK, dV of the tile are written (bf16) once at the end — no cross-CTA reduction.
+//  bwd_q_kernel — one CTA per (Q tile, query head); loops over K/V tiles:
+//      S = Q̃ Kᵀ, dP = dO Vᵀ (SS) -> dŜ (bf16, TMEM) -> dQ̃ += dŜ K (TS, B = K MN-major)
+//    dQ̃ (fp32) goes to a workspace; fold_all_kernel (bwd.cu) folds it onto the representatives.
+//
+// Every operand layout and descriptor is the one the forward kernel (attn.cu) uses: natural
+// [rows][d] tiles in 64-column SWIZZLE_128B boxes serve as K-major operands (rows = M or N,
+// d = K) and as MN-major B operands (rows = K, d = N). d in {64, 128}.
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "internal.h"
+#include "ptx.cuh"
+
+namespace da {
+namespace {
+
+constexpr int T = 128;            // rows per tile (queries or keys)
+constexpr int kThreadsB = 384;    // warp 0 TMA, warp 1 MMA, warps 4..11 elementwise
+constexpr uint32_t kSw = kSw128;
+
+enum { BB_KV = 0, BB_FULL = 1, BB_EMPTY = 3, BB_SFULL = 5, BB_PFULL = 6, BB_DONE = 7, BB_TMEM = 8, BB_N = 9 };
+
+template <int D>
+struct BCfg {
+  static constexpr int TILE = T * D * 2;  // one [128][d] bf16 tile (D/64 boxes of 16 KB)
+  static constexpr int VEC = 1024;        // lse + D vectors of a Q tile (2 x 128 fp32)
+  // kv kernel: K, V stationary + 2-stage ring of (Q̃, dO, vec)
+  static constexpr int KV_SMEM = 2 * TILE + 2 * (2 * TILE + VEC) + 256 + 1024;
+  // q kernel: Q̃, dO stationary + 2-stage ring of (K, V)
+  static constexpr int Q_SMEM = 2 * TILE + 2 * (2 * TILE) + 256 + 1024;
+};
+
+DA_DEV uint64_t kmaj(uint32_t base, int kk) {  // K-major operand of a [128][d] tile: K-step kk
+  return make_sdesc(base + (kk / 4) * (T * 128) + (kk % 4) * 32, 16, 1024, kSw);
+}
+DA_DEV uint64_t mnmaj(uint32_t base, int kk) {  // MN-major B operand: 16 K-rows per step
+  return make_sdesc(base + kk * 2048, T * 128, 1024, kSw);
+}
+DA_DEV void load_tile(uint8_t* dst, const CUtensorMap* m, uint64_t* bar, int D, int row, int plane) {
+  for (int bx = 0; bx < D / 64; ++bx) tma_load_3d(dst + bx * (T * 128), m, bar, bx * 64, row, plane);
+}
+
+// ------------------------------------------------------------------------------------ dK, dV
+template <int D>
+__global__ void __launch_bounds__(kThreadsB, 1)
+    bwd_kv_kernel(const __grid_constant__ CUtensorMap tmQt, const __grid_constant__ CUtensorMap tmdO,
+                  const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+                  const BwdFusedArgs a) {
+  using C = BCfg<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  uint8_t* sK = smem;
+  uint8_t* sV = sK + C::TILE;
+  uint8_t* ring = sV + C::TILE;  // stage s: Q̃ tile, dO tile, vec
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + 2 * (2 * C::TILE + C::VEC));
+  uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(bars + BB_TMEM);
+  const int warp = warp_id(), lane = lane_id();
+  const int kt = blockIdx.x, bhkv = blockIdx.y;
+  const int rep = a.H / a.Hkv;
+  const int b = bhkv / a.Hkv, hk = bhkv % a.Hkv;
+  const int nqt = (a.N + T - 1) / T;
+  const int qt_first = a.causal ? kt : 0;  // causal: queries >= keys
+  const int per_head = nqt - qt_first;
+  const int ntiles = rep * per_head;
+  auto tile_of = [&](int n, int* bh, int* qt) {
+    *bh = b * a.H + hk * rep + n / per_head;
+    *qt = qt_first + n % per_head;
+  };
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[BB_KV], 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&bars[BB_FULL + s], 1);
+      mbar_init(&bars[BB_EMPTY + s], 1);
+    }
+    mbar_init(&bars[BB_SFULL], 1);
+    mbar_init(&bars[BB_PFULL], 256);
+    mbar_init(&bars[BB_DONE], 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    tmem_alloc(tmem_ptr, 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_ptr;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(&bars[BB_KV], 2 * C::TILE);
+      load_tile(sK, &tmK, &bars[BB_KV], D, kt * T, bhkv);
+      load_tile(sV, &tmV, &bars[BB_KV], D, kt * T, bhkv);
+      for (int n = 0; n < ntiles; ++n) {
+        const int s = n & 1;
+        int bh, qt;
+        tile_of(n, &bh, &qt);
+        mbar_wait(&bars[BB_EMPTY + s], ((n >> 1) & 1) ^ 1);
+        uint8_t* st = ring + s * (2 * C::TILE + C::VEC);
+        mbar_arrive_expect_tx(&bars[BB_FULL + s], 2 * C::TILE + C::VEC);
+        load_tile(st, &tmQt, &bars[BB_FULL + s], D, qt * T, bh);
+        load_tile(st + C::TILE, &tmdO, &bars[BB_FULL + s], D, qt * T, bh);
+        bulk_g2s(st + 2 * C::TILE, a.lse_pad + ((size_t)bh * a.N_pad + qt * T), 512, &bars[BB_FULL + s]);
+        bulk_g2s(st + 2 * C::TILE + 512, a.D_pad + ((size_t)bh * a.N_pad + qt * T), 512, &bars[BB_FULL + s]);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t IS = make_idesc_bf16(T, T, false, false);   // Sᵀ, dPᵀ
+      constexpr uint32_t IG = make_idesc_bf16(T, D, false, true);    // dV, dK (B MN-major)
+      mbar_wait(&bars[BB_KV], 0);
+      tc_fence_after();
+      const uint32_t kb = smem_u32(sK), vb = smem_u32(sV);
+      for (int n = 0; n < ntiles; ++n) {
+        const int s = n & 1;
+        mbar_wait(&bars[BB_FULL + s], (n >> 1) & 1);
+        tc_fence_after();
+        const uint32_t qb = smem_u32(ring + s * (2 * C::TILE + C::VEC)), ob = qb + C::TILE;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) mma_ss(tmem, kmaj(kb, kk), kmaj(qb, kk), IS, kk > 0);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) mma_ss(tmem + 128, kmaj(vb, kk), kmaj(ob, kk), IS, kk > 0);
+        mma_commit(&bars[BB_SFULL]);
+        mbar_wait(&bars[BB_PFULL], n & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < T / 16; ++kk) {
+          // Pᵀ / dŜᵀ of queries [64h, 64h + 64) live in columns [64h, 64h + 32) of the Sᵀ / dPᵀ range
+          const uint32_t pc = (uint32_t)((kk >> 2) * 64 + (kk & 3) * 8);
+          mma_ts(tmem + 256, tmem + pc, mnmaj(ob, kk), IG, (n > 0 || kk > 0) ? 1u : 0u);
+          mma_ts(tmem + 384, tmem + 128 + pc, mnmaj(qb, kk), IG, (n > 0 || kk > 0) ? 1u : 0u);
+        }
+        mma_commit(&bars[BB_EMPTY + s]);
+      }
+      mma_commit(&bars[BB_DONE]);
+    }
+  } else if (warp >= 4) {
+    const int half = (warp - 4) >> 2, quad = warp & 3;
+    const int key = kt * T + quad * 32 + lane;  // this thread's key row (TMEM lane)
+    const uint32_t lb = (uint32_t)(quad * 32) << 16;
+    const float sl2 = a.scale * 1.4426950408889634f, l2e = 1.4426950408889634f;
+    for (int n = 0; n < ntiles; ++n) {
+      const int s = n & 1;
+      int bh, qt;
+      tile_of(n, &bh, &qt);
+      mbar_wait(&bars[BB_SFULL], n & 1);
+      tc_fence_after();
+      const float* vec = reinterpret_cast<const float*>(ring + s * (2 * C::TILE + C::VEC) + 2 * C::TILE);
+      // two 32-query chunks of this half: Sᵀ, dPᵀ chunk -> Pᵀ, dŜᵀ (bf16) into the first halves of
+      // the chunk's own column ranges (chunk c of half h: queries 64h + 32c + [0, 32))
+#pragma unroll
+      for (int c2 = 0; c2 < 2; ++c2) {
+        uint32_t sr[32], pr[32];
+        tmem_ld32(tmem + lb + 64 * half + 32 * c2, sr);
+        tmem_ld32(tmem + lb + 128 + 64 * half + 32 * c2, pr);
+        tmem_ld_wait();
+        const int q0 = qt * T + 64 * half + 32 * c2;
+        const float* lv = vec + 64 * half + 32 * c2;
+        const float* dv = vec + 128 + 64 * half + 32 * c2;
+        uint32_t pk[16], dk2[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          float p2[2], d2[2];
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int c = 2 * e + u;
+            float p = ex2(__uint_as_float(sr[c]) * sl2 - lv[c] * l2e);
+            if (a.causal && key > q0 + c) p = 0.f;
+            p2[u] = p;
+            d2[u] = p * (__uint_as_float(pr[c]) - dv[c]) * a.scale;
+          }
+          pk[e] = pack_bf16x2(p2[0], p2[1]);
+          dk2[e] = pack_bf16x2(d2[0], d2[1]);
+        }
+        // into this half's own columns (no other warp reads them): no race with the other half
+        tmem_st16(tmem + lb + 64 * half + 16 * c2, pk);
+        tmem_st16(tmem + lb + 128 + 64 * half + 16 * c2, dk2);
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(&bars[BB_PFULL]);
+    }
+    // epilogue: dV, dK rows of this key (each half writes d/2 columns)
+    mbar_wait(&bars[BB_DONE], 0);
+    tc_fence_after();
+    for (int which = 0; which < 2; ++which) {
+      uint16_t* dst = (which == 0 ? a.dv : a.dk) + ((size_t)bhkv * a.N + key) * D + half * (D / 2);
+      const uint32_t src = tmem + lb + (which == 0 ? 256 : 384) + half * (D / 2);
+#pragma unroll
+      for (int c = 0; c < D / 64; ++c) {
+        uint32_t r[32];
+        tmem_ld32(src + 32 * c, r);
+        tmem_ld_wait();
+        if (key < a.N) {
+          uint4* o = reinterpret_cast<uint4*>(dst + 32 * c);
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            o[e] = make_uint4(pack_bf16x2(__uint_as_float(r[8 * e]), __uint_as_float(r[8 * e + 1])),
+                              pack_bf16x2(__uint_as_float(r[8 * e + 2]), __uint_as_float(r[8 * e + 3])),
+                              pack_bf16x2(__uint_as_float(r[8 * e + 4]), __uint_as_float(r[8 * e + 5])),
+                              pack_bf16x2(__uint_as_float(r[8 * e + 6]), __uint_as_float(r[8 * e + 7])));
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+// ------------------------------------------------------------------------------------ dQ̃
+template <int D>
+__global__ void __launch_bounds__(kThreadsB, 1)
+    bwd_q_kernel(const __grid_constant__ CUtensorMap tmQt, const __grid_constant__ CUtensorMap tmdO,
+                 const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
+                 const BwdFusedArgs a) {
+  using C = BCfg<D>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
+  uint8_t* sQ = smem;
+  uint8_t* sO = sQ + C::TILE;
+  uint8_t* ring = sO + C::TILE;  // stage s: K tile, V tile
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ring + 2 * (2 * C::TILE));
+  uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(bars + BB_TMEM);
+  const int warp = warp_id(), lane = lane_id();
+  const int qt = blockIdx.x, bh = blockIdx.y;
+  const int b = bh / a.H, h = bh % a.H, bhkv = b * a.Hkv + h / (a.H / a.Hkv);
+  const int nkt = (a.N + T - 1) / T;
+  const int ntiles = a.causal ? min(qt + 1, nkt) : nkt;
+  if (threadIdx.x == 0) {
+    mbar_init(&bars[BB_KV], 1);
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&bars[BB_FULL + s], 1);
+      mbar_init(&bars[BB_EMPTY + s], 1);
+    }
+    mbar_init(&bars[BB_SFULL], 1);
+    mbar_init(&bars[BB_PFULL], 256);
+    mbar_init(&bars[BB_DONE], 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) {
+    tmem_alloc(tmem_ptr, 512);
+    tmem_relinquish();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_ptr;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      mbar_arrive_expect_tx(&bars[BB_KV], 2 * C::TILE);
+      load_tile(sQ, &tmQt, &bars[BB_KV], D, qt * T, bh);
+      load_tile(sO, &tmdO, &bars[BB_KV], D, qt * T, bh);
+      for (int n = 0; n < ntiles; ++n) {
+        const int s = n & 1;
+        mbar_wait(&bars[BB_EMPTY + s], ((n >> 1) & 1) ^ 1);
+        uint8_t* st = ring + s * (2 * C::TILE);
+        mbar_arrive_expect_tx(&bars[BB_FULL + s], 2 * C::TILE);
+        load_tile(st, &tmK, &bars[BB_FULL + s], D, n * T, bhkv);
+        load_tile(st + C::TILE, &tmV, &bars[BB_FULL + s], D, n * T, bhkv);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t IS = make_idesc_bf16(T, T, false, false);
+      constexpr uint32_t IG = make_idesc_bf16(T, D, false, true);
+      mbar_wait(&bars[BB_KV], 0);
+      tc_fence_after();
+      const uint32_t qb = smem_u32(sQ), ob = smem_u32(sO);
+      for (int n = 0; n < ntiles; ++n) {
+        const int s = n & 1;
+        mbar_wait(&bars[BB_FULL + s], (n >> 1) & 1);
+        tc_fence_after();
+        const uint32_t kb = smem_u32(ring + s * (2 * C::TILE)), vb = kb + C::TILE;
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) mma_ss(tmem, kmaj(qb, kk), kmaj(kb, kk), IS, kk > 0);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk) mma_ss(tmem + 128, kmaj(ob, kk), kmaj(vb, kk), IS, kk > 0);
+        mma_commit(&bars[BB_SFULL]);
+        mbar_wait(&bars[BB_PFULL], n & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < T / 16; ++kk)
+          mma_ts(tmem + 256, tmem + (uint32_t)((kk >> 2) * 64 + (kk & 3) * 8), mnmaj(kb, kk), IG,
+                 (n > 0 || kk > 0) ? 1u : 0u);
+        mma_commit(&bars[BB_EMPTY + s]);
+      }
+      mma_commit(&bars[BB_DONE]);
+    }
+  } else if (warp >= 4) {
+    const int half = (warp - 4) >> 2, quad = warp & 3;
+    const int row = qt * T + quad * 32 + lane;
+    const uint32_t lb = (uint32_t)(quad * 32) << 16;
+    const float sl2 = a.scale * 1.4426950408889634f;
+    const float lse2 = a.lse_pad[(size_t)bh * a.N_pad + row] * 1.4426950408889634f;
+    const float dd = a.D_pad[(size_t)bh * a.N_pad + row];
+    for (int n = 0; n < ntiles; ++n) {
+      mbar_wait(&bars[BB_SFULL], n & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int c2 = 0; c2 < 2; ++c2) {
+        uint32_t sr[32], pr[32];
+        tmem_ld32(tmem + lb + 64 * half + 32 * c2, sr);
+        tmem_ld32(tmem + lb + 128 + 64 * half + 32 * c2, pr);
+        tmem_ld_wait();
+        const int k0 = n * T + 64 * half + 32 * c2;
+        uint32_t dk2[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+          float d2[2];
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int c = 2 * e + u;
+            float p = ex2(__uint_as_float(sr[c]) * sl2 - lse2);
+            if (a.causal && k0 + c > row) p = 0.f;
+            d2[u] = p * (__uint_as_float(pr[c]) - dd) * a.scale;
+          }
+          dk2[e] = pack_bf16x2(d2[0], d2[1]);
+        }
+        tmem_st16(tmem + lb + 64 * half + 16 * c2, dk2);
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(&bars[BB_PFULL]);
+    }
+    mbar_wait(&bars[BB_DONE], 0);
+    tc_fence_after();
+    float* dst = a.dqt + ((size_t)bh * a.N + row) * D + half * (D / 2);
+#pragma unroll
+    for (int c = 0; c < D / 64; ++c) {
+      uint32_t r[32];
+      tmem_ld32(tmem + lb + 256 + half * (D / 2) + 32 * c, r);
+      tmem_ld_wait();
+      if (row < a.N) {
+        float4* o = reinterpret_cast<float4*>(dst + 32 * c);
+#pragma unroll
+        for (int e = 0; e < 8; ++e)
+          o[e] = make_float4(__uint_as_float(r[4 * e]), __uint_as_float(r[4 * e + 1]), __uint_as_float(r[4 * e + 2]),
+                             __uint_as_float(r[4 * e + 3]));
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+template <int D>
+cudaError_t launch_fused_t(const BwdFusedArgs& a, cudaStream_t st) {
+  using C = BCfg<D>;
+  cudaError_t e = cudaFuncSetAttribute(bwd_kv_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::KV_SMEM);
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(bwd_q_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::Q_SMEM);
+  if (e != cudaSuccess) return e;
+  const int nt = (a.N + T - 1) / T;
+  bwd_kv_kernel<D><<<dim3(nt, a.BHkv), kThreadsB, C::KV_SMEM, st>>>(*a.tmQt, *a.tmdO, *a.tmK, *a.tmV, a);
+  e = cudaGetLastError();
+  if (e != cudaSuccess) return e;
+  bwd_q_kernel<D><<<dim3(nt, a.BH), kThreadsB, C::Q_SMEM, st>>>(*a.tmQt, *a.tmdO, *a.tmK, *a.tmV, a);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_bwd_fused(const BwdFusedArgs& a, cudaStream_t st) {
+  if (a.d == 64) return launch_fused_t<64>(a, st);
+  if (a.d == 128) return launch_fused_t<128>(a, st);
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace da

@@ -69,7 +69,8 @@ struct BwdArgs {
   float scale;
   int R, nb;              // query rows per chunk, heads per batched GEMM
   uint16_t* qt;           // [BH][N][d] Q̃
-  float* D;               // [BH][N]
+  float* D;               // [BH][Dstride]
+  int Dstride;            // N (cuBLAS path) or N_pad (fused path)
   float *S, *dP;          // [nb][R][N] fp32
   uint16_t *P16, *dS16;   // [nb][R][N] bf16
   float* dqt;             // [nb][R][d]
@@ -78,6 +79,23 @@ struct BwdArgs {
   void** dev_ptrs;        // device copy
 };
 int run_backward(const BwdArgs& a, void* cublas_handle, cudaStream_t st);  // 0 = ok
+
+// Fused tcgen05 backward (bwd_fused.cu), d in {64, 128}. Maps: Q̃, dO [BH][N][d]; K, V
+// [BHkv][N][d], all 64-column SWIZZLE_128B boxes of 128 rows.
+struct BwdFusedArgs {
+  const CUtensorMap *tmQt, *tmdO, *tmK, *tmV;
+  const float* lse_pad;  // [BH][N_pad] (+inf past N)
+  const float* D_pad;    // [BH][N_pad] (0 past N)
+  float* dqt;            // [BH][N][d] fp32 dQ̃
+  uint16_t *dk, *dv;     // [BHkv][N][d] bf16 outputs
+  int BH, BHkv, H, Hkv, N, N_pad, d, causal;
+  float scale;
+};
+cudaError_t launch_bwd_fused(const BwdFusedArgs& a, cudaStream_t st);
+// bwd.cu helpers for the fused path
+cudaError_t launch_bwd_prologue(const BwdArgs& a, const float* lse, float* lse_pad, int N_pad, cudaStream_t st);
+cudaError_t launch_fold_all(const float* dqt, const uint8_t* perm, uint16_t* dq, int BH, int N, int d, int G,
+                            int nqb, int block_l, cudaStream_t st);
 cudaError_t launch_convert_bf16(const float* src, uint16_t* dst, size_t n, cudaStream_t st);
 
 // Which kernel flavour: DISTR with (d, G, HB) or exact with d.

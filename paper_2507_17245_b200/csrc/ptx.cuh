@@ -60,6 +60,13 @@ DA_DEV void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar, int c0
 
 // ------------------------------------------------------------------------------------ tcgen05
 // TMEM address: bits [31:16] lane, [15:0] column (32-bit columns).
+// 1-D bulk copy global -> shared, completion counted on an mbarrier (bytes % 16 == 0, 16-B aligned).
+DA_DEV void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   smem_u32(dst)),
+               "l"(src), "r"(bytes), "r"(smem_u32(bar))
+               : "memory");
+}
 DA_DEV void tmem_alloc(uint32_t* dst_smem, uint32_t ncols) {  // whole warp
   asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(dst_smem)),
                "r"(ncols)

@@ -75,3 +75,15 @@ def test_backward_ragged_and_multichunk(N):
     res = run(cfg(N=N, H=2, H_kv=1, causal=True))
     for name, (rel, mx) in res.items():
         assert rel <= 1e-2 and mx <= 3e-2, (N, name, rel, mx)
+
+
+def test_cublas_path_matches_fused(monkeypatch):
+    # the first (cuBLAS, materialised scores) backward stays available for d = 32 and as a
+    # cross-check of the fused tcgen05 kernels (DA_BWD_CUBLAS selects it for any d)
+    c = cfg(N=700, causal=True)
+    fused = run(c)
+    monkeypatch.setenv("DA_BWD_CUBLAS", "1")
+    cub = run(c)
+    for name in ("dq", "dk", "dv"):
+        for res in (fused, cub):
+            assert res[name][0] <= 1e-2 and res[name][1] <= 3e-2, (name, res[name])
