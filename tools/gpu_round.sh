@@ -1,5 +1,6 @@
 #!/bin/bash
-# One GPU session: tests, smoke, bench, ncu launch list + full capture. Logs under gpurun_out/.
+# One GPU session: tests, smoke, bench, ncu launch list + full captures (forward attention, K^T
+# prep, fused backward), per-config sweep, Pareto sweep, backward timing. Logs under gpurun_out/.
 set -x
 O=gpurun_out
 mkdir -p $O
@@ -13,4 +14,8 @@ timeout -s KILL 900 python bench.py > $O/bench.log 2>&1; echo "bench rc=$?" >> $
 timeout -s KILL 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"prep_kernel|attn_kernel|convert_kernel" -c 60 --csv --log-file $O/launches.csv python bench.py --steps 2 --warmup 3 --no-e2e --no-cpu --no-parity > $O/ncu_launches.log 2>&1
 timeout -s KILL 900 ncu --set full --clock-control none --import-source on -k regex:attn_kernel -s 3 -c 1 -o $O/prof_attn -f python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --no-parity > $O/ncu_full_attn.log 2>&1
 timeout -s KILL 600 ncu --set full --clock-control none --import-source on -k regex:prep_kernel -s 3 -c 1 -o $O/prof_prep -f python bench.py --steps 1 --warmup 3 --no-e2e --no-cpu --no-parity > $O/ncu_full_prep.log 2>&1
+timeout -s KILL 600 python tools/sweep.py > $O/sweep.json 2> $O/sweep.err
+timeout -s KILL 900 python tools/pareto.py > $O/pareto.json 2> $O/pareto.err
+timeout -s KILL 600 python tools/bench_bwd.py > $O/bwd.json 2> $O/bwd.err
+timeout -s KILL 600 ncu --set full --clock-control none --import-source on -k regex:"bwd_kv_kernel|bwd_q_kernel" -c 2 -o $O/prof_bwd -f python tools/bench_bwd.py > $O/ncu_full_bwd.log 2>&1
 ls -la $O

@@ -29,10 +29,10 @@ ap.add_argument("--rounds", type=int, default=3)
 args = ap.parse_args()
 L = _native.lib()
 
-VARIANTS = [(d, l, g) for d in (64, 128) for l in (64, 128) for g in (1, 2, 4, 8)
-            if d % g == 0 and (128 // l) * d // g in range(16, 129) and (g != 8 or d == 128)]
+VARIANTS = [(d, l, g) for d in (32, 64, 128) for l in (64, 128) for g in (1, 2, 4, 8)
+            if d % g == 0 and d // g >= 16 and (128 // l) * d // g in range(16, 129)]
 # global grouping (one LSH over all N rows per head): block_l = 0 marks it
-VARIANTS += [(d, 0, g) for d in (64, 128) for g in (2, 4, 8) if d // g >= 16]
+VARIANTS += [(d, 0, g) for d in (32, 64, 128) for g in (2, 4, 8) if d // g >= 16]
 DISTS = ("normal", "clustered", "block_clustered")
 
 
