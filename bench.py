@@ -119,6 +119,15 @@ def oracle_sample_time(cfg, q, k, v, G, n_items, seed=0):
     return time.perf_counter() - t0, len(items), oracle.num_threads()
 
 
+def bench_config(cfg, G, B_per_rank, world, shard):
+    """The `config` object of the JSON line (identical for both arms)."""
+    return {"workload": f"{cfg.name}: B={cfg.B} H={cfg.H} N={cfg.N} d={cfg.d} block_l={cfg.block_l} "
+                        f"G*={G} bf16 {'causal' if cfg.causal else 'non-causal'}",
+            "B_per_rank": B_per_rank,
+            "parallelism": (f"Q-tile-pair-sharded x{world}" if shard == "q" else f"(b,h)-sharded x{world}"),
+            "l2": "inputs (17 GB) larger than L2, no flush"}
+
+
 def run_reference(args, cfg):
     """Reference arm: the CPU oracle as it stands, bounded samples, extrapolated to the job."""
     rank, world, _ = dist_env()
@@ -145,8 +154,7 @@ def run_reference(args, cfg):
         "impl": "reference", "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": {"workload": cfg.name, "B": B, "H": cfg.H, "N": cfg.N,
-                                        "d": cfg.d, "block_l": cfg.block_l, "group_size": G},
+        "data": "synthetic", "config": bench_config(cfg, G, B, world, "bh"),
         "cpu_baseline": {"value": ms, "unit": "ms", "cores": oracle.num_threads(),
                          "kind": "oracle", "sample": sample},
         "e2e": {"value": ms, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -311,13 +319,7 @@ def main():
             "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": {"workload": f"{cfg.name}: B={cfg.B} H={cfg.H} N={cfg.N} d={cfg.d} "
-                                   f"block_l={cfg.block_l} G*={G} bf16 "
-                                   f"{'causal' if cfg.causal else 'non-causal'}",
-                       "B_per_rank": B,
-                       "parallelism": (f"Q-tile-pair-sharded x{world}" if args.shard == "q"
-                                       else f"(b,h)-sharded x{world}"),
-                       "l2": "inputs (17 GB) larger than L2, no flush"},
+            "config": bench_config(cfg, G, B, world, args.shard),
             "exact_ms": ex_ms, "speedup_vs_exact": ex_ms / ms,
             "attn_kernel_ms": attn_ms, "prep_kernel_ms": prep_ms, "exact_kernel_ms": ex_attn_ms,
             "tflops_executed": exec_f * world / (ms * 1e-3) / 1e12,
