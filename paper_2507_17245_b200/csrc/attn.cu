@@ -26,6 +26,11 @@
 #include "internal.h"
 #include "ptx.cuh"
 
+#ifndef DA_HASH_UNROLL
+#define DA_HASH_UNROLL 8
+#endif
+constexpr int kHashUnroll = DA_HASH_UNROLL;  // rows of the projection chain unrolled
+
 namespace da {
 namespace {
 
@@ -153,7 +158,7 @@ DA_DEV void qhat_prologue(const AttnArgs& args, uint64_t* bars, const uint8_t* s
 #pragma unroll
       for (int m = 0; m < 4; ++m) ya[m] = yb[m] = make_float2(0.0f, 0.0f);
       const float* pr = proj_t + 8 * kh;
-#pragma unroll 2
+#pragma unroll kHashUnroll
       for (int r = 0; r < rows; ++r) {
         const uint32_t q2 = *reinterpret_cast<const uint32_t*>(sQ + q_off(t, hb * L + r, c));
         const float qa = __uint_as_float(q2 << 16), qb = __uint_as_float(q2 & 0xFFFF0000u);

@@ -10,6 +10,7 @@ for v in "$@"; do
   for e in ${EMUS:-0 2}; do
     DA_EMU=$e timeout -s KILL 120 python bench.py --steps 5 --no-e2e --no-cpu --no-parity > $O/bench_${v}_e$e.log 2>&1
   done
+  [ -n "$SWEEP" ] && timeout -s KILL 300 python tools/sweep.py --only "$SWEEP" > $O/sweep_$v.json 2>&1
   timeout -s KILL 60 python tools/trace.py distr > $O/trace_${v}_distr.log 2>&1
   timeout -s KILL 60 python tools/trace.py exact > $O/trace_${v}_exact.log 2>&1
 done

@@ -16,11 +16,14 @@ from synth import CONFIGS, C4_SWEEP_N, make_qkv
 ap = argparse.ArgumentParser()
 ap.add_argument("--steps", type=int, default=10)
 ap.add_argument("--warmup", type=int, default=3)
+ap.add_argument("--only", default="", help="comma-separated case-name prefixes (default: all)")
 args = ap.parse_args()
 L = _native.lib()
 cases = [("C1", CONFIGS["C1"]), ("C2", CONFIGS["C2"]), ("C3", CONFIGS["C3"])]
 cases += [(f"C4 N={n} G*={g}", CONFIGS["C4"].with_(N=n, group_size=g)) for n in C4_SWEEP_N for g in (2, 4)]
 cases += [("C5 1-GPU", CONFIGS["C5"])]
+if args.only:
+    cases = [c for c in cases if any(c[0].startswith(p) for p in args.only.split(","))]
 
 
 def timed(fn):
