@@ -236,15 +236,19 @@ int current_device(int* dev) {
 // Measured on B200 (profiles/r01_v4): the exp phase of a tile is MUFU-bound
 // (16 ex2/clk/SM); moving 2/8 of the pairs to the FMA pipe shortens it by ~10 % and helps the
 // distr kernel, whose tensor-core block is shorter than the softmax; the exact kernel is then
-// co-bound by its longer tensor block and loses (power draw), so it keeps 0. DA_EMU overrides
-// (0, 2, 3, 4) for tuning.
+// co-bound by its longer tensor block and loses (power draw), so it keeps 0. DA_EMU (distr) and
+// DA_EMU_EXACT (exact) override (0, 2, 3, 4) for tuning.
 int default_emu(const Plan& P, bool distr) {
-  static int env = [] {
-    const char* e = getenv("DA_EMU");
-    return e ? atoi(e) : -1;
-  }();
+  static const int env[2] = {[] {
+                               const char* e = getenv("DA_EMU_EXACT");
+                               return e ? atoi(e) : -1;
+                             }(),
+                             [] {
+                               const char* e = getenv("DA_EMU");
+                               return e ? atoi(e) : -1;
+                             }()};
   (void)P;
-  if (env >= 0) return env;
+  if (env[distr ? 1 : 0] >= 0) return env[distr ? 1 : 0];
   return distr ? 2 : 0;
 }
 

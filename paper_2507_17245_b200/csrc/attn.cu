@@ -30,14 +30,40 @@
 #define DA_HASH_UNROLL 8
 #endif
 constexpr int kHashUnroll = DA_HASH_UNROLL;  // rows of the projection chain unrolled
+#ifndef DA_SPLIT
+#define DA_SPLIT 2
+#endif
+#ifndef DA_WARP_ARRIVE
+#define DA_WARP_ARRIVE 0
+#endif
+#ifndef DA_DIAG_NOFUSE
+#define DA_DIAG_NOFUSE 0
+#endif
+#ifndef DA_EMU_SPREAD
+#define DA_EMU_SPREAD 0
+#endif
+// Consumer-release barriers (P ready, K̂ ready, K stage free, Q̂ built) take one arrival per warp
+// (lane 0 after __syncwarp) instead of one per thread. Measured on B200: no gain (the MMA warp's
+// wake-up after the last arrival stays ~300 clk), so off by default.
+constexpr int kArrive = DA_WARP_ARRIVE ? 32 : 1;  // threads per arrival
+// Softmax warps per query row: the 128 key columns of a tile are split SPLIT ways (4 x SPLIT
+// softmax warps, 128/SPLIT columns per thread).
+constexpr int kSplit = DA_SPLIT;
+static_assert(kSplit == 2 || kSplit == 4, "softmax split");
 
 namespace da {
 namespace {
 
-// 384 threads (exact: TMA/MMA warpgroup + 2 softmax warpgroups) or 512 (distr: + fusion warpgroup)
+// TMA/MMA warpgroup + SPLIT softmax warpgroups (+ the fusion warpgroup for distr):
+// SPLIT = 4 -> 640 threads (exact) / 768 (distr).
+constexpr int kSoftmaxWarps = 4 * kSplit;
+constexpr int kSoftmaxThreads = 32 * kSoftmaxWarps;
+constexpr int kCW = 128 / kSplit;  // key columns per softmax thread
 template <bool DISTR>
-constexpr int threads_of() { return DISTR ? 512 : 384; }
+constexpr int threads_of() { return 128 + kSoftmaxThreads + (DISTR ? 128 : 0); }
 constexpr int kFusionThreads = 128;
+constexpr int kWorkers = kSoftmaxThreads + kFusionThreads;  // distr: threads running qhat_prologue
+constexpr int kXchBytes = 6 * kSplit * 128 * 4;  // row max [2 parity][2 t][SPLIT][128] + sums [2 t][SPLIT][128]
 constexpr int BM = 128;  // query rows per tile (UMMA M)
 constexpr int BN = 128;  // keys per tile (UMMA N of S, K of PV)
 constexpr uint32_t kTmemCols = 512;
@@ -59,7 +85,7 @@ struct Cfg {
   static constexpr int KH_BYTES = DISTR ? DR * BN * 2 : 0;
   static constexpr int al(int x) { return (x + 1023) / 1024 * 1024; }
   static constexpr int bytes(int ns, int nkh) {
-    return al(2 * A_BYTES) + ns * (K_BYTES + V_BYTES) + 2 * nkh * KH_BYTES + 1024 + 6144;
+    return al(2 * A_BYTES) + ns * (K_BYTES + V_BYTES) + 2 * nkh * KH_BYTES + 1024 + 256 + kXchBytes;
   }
   // Deepest K/V ring (NS) and K̂ ring (NKH) that fit the 227 KB of shared memory.
   static constexpr int NKH = !DISTR ? 0 : (bytes(2, 2) <= kSmemMax ? 2 : 1);
@@ -70,7 +96,7 @@ struct Cfg {
   static constexpr int OFF_KH = OFF_V + NS * V_BYTES;
   static constexpr int OFF_PERM = OFF_KH + 2 * NKH * KH_BYTES;
   static constexpr int OFF_BAR = OFF_PERM + 2 * 2 * 128;
-  static constexpr int SMEM = OFF_BAR + 256 + 6144 + 1024;  // barriers, row-max/sum exchange, align slack
+  static constexpr int SMEM = OFF_BAR + 256 + kXchBytes + 1024;  // barriers, row-max/sum exchange, align slack
   static constexpr uint32_t A_LAYOUT = A_SW == 128 ? kSw128 : (A_SW == 64 ? kSw64 : kSw32);
   static constexpr int A_SWB = A_SW == 128 ? 3 : (A_SW == 64 ? 2 : 1);  // Swizzle<B,4,3> bits
   // distr: the natural Q tiles (K-major SW128 boxes, 128 rows x d) are staged for the in-CTA
@@ -98,10 +124,21 @@ enum {
   B_SFULL = 17,   // +t
   B_PFULL = 19,   // +t
   B_OFULL = 21,   // +t
-  B_QHAT = 23,    // distr: Q̂ of both tiles built in sA (384 hashing threads arrive)
+  B_QHAT = 23,    // distr: Q̂ of both tiles built in sA (kWorkers hashing threads arrive)
   B_TMEMPTR = 24,
   B_COUNT = 25
 };
+
+// Release arrival of a whole warp: every lane's prior writes (and fences) are ordered before lane
+// 0's arrive by the warp barrier (kArrive == 32), or every thread arrives (kArrive == 1).
+DA_DEV void warp_arrive(uint64_t* bar) {
+  if constexpr (kArrive == 32) {
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(bar);
+  } else {
+    mbar_arrive(bar);
+  }
+}
 
 // Swizzle<B,4,3>: XOR byte-address bits [4, 4+B) with bits [7, 7+B) — the TMA / UMMA
 // SWIZZLE_{32,64,128}B layouts (B = 1, 2, 3), valid inside 1024-byte aligned regions.
@@ -115,8 +152,8 @@ DA_DEV uint32_t inverse_gray16(uint32_t p) {
   return p & 0xFFFFu;
 }
 
-// LSH + grouping + sampling of the CTA's two Q tiles (§3.2-3.3), run by the 384
-// worker threads (warps 4-15) before their roles start. Same arithmetic as prep.cu hash_cta
+// LSH + grouping + sampling of the CTA's two Q tiles (§3.2-3.3), run by the kWorkers
+// worker threads (the softmax and fusion warps) before their roles start. Same arithmetic as prep.cu hash_cta
 // (bit-exact contract with the oracle: fp32 fma chain in ascending rows from +0, strict y > 0,
 // LSB = projection row 0, inverse Gray, stable rank by (bucket, column)):
 //   staged Q (natural, SW128 K-major boxes) -> y[16] per (tile, hash block, column) -> perm_s
@@ -127,12 +164,12 @@ DA_DEV void qhat_prologue(const AttnArgs& args, uint64_t* bars, const uint8_t* s
                           uint8_t* perm_s, int bh, int qt0, int ntile, int ht, long long* trace) {
 #define PT(i) if (trace && ht == 0) trace[15 * 256 + (i)] = clock64();
   PT(0)
-  constexpr int NW = 384;
+  constexpr int NW = kWorkers;
   constexpr int DG = D / G;
   const int L = args.block_l;
   float* proj_t = reinterpret_cast<float*>(scratch);           // [l][16]
   uint32_t* key_s = reinterpret_cast<uint32_t*>(scratch + 8192);  // [2][HB][D] keys + [2][HB][D][2] u8 parts
-  auto wsync = [] { asm volatile("bar.sync 5, 384;" ::: "memory"); };
+  auto wsync = [] { asm volatile("bar.sync 5, %0;" ::"n"(kWorkers) : "memory"); };
   // byte offset of staged Q(t, r, c): box c / RB, RB*2-byte rows, SWIZZLE_{RB*2}B
   auto q_off = [&](int t, int r, int c) -> uint32_t {
     return (uint32_t)(t * C::QT_BYTES + (c / C::RB) * (BM * C::RB * 2)) +
@@ -251,7 +288,7 @@ DA_DEV void qhat_prologue(const AttnArgs& args, uint64_t* bars, const uint8_t* s
     }
   }
   fence_proxy_async_smem();
-  mbar_arrive(&bars[B_QHAT]);
+  warp_arrive(&bars[B_QHAT]);
   PT(4)
 #undef PT
 }
@@ -301,20 +338,20 @@ __global__ void __launch_bounds__(threads_of<DISTR>(), 1)
 
   if (threadIdx.x == 0) {
     mbar_init(&bars[B_Q], 1);
-    mbar_init(&bars[B_QHAT], 384);
+    mbar_init(&bars[B_QHAT], kWorkers / kArrive);
     for (int s = 0; s < NS; ++s) {
       mbar_init(&bars[B_KFULL + s], 1);
-      mbar_init(&bars[B_KEMPTY + s], DISTR ? kFusionThreads : 1);
+      mbar_init(&bars[B_KEMPTY + s], DISTR ? kFusionThreads / kArrive : 1);
       mbar_init(&bars[B_VFULL + s], 1);
       mbar_init(&bars[B_VEMPTY + s], 1);
     }
     for (int t = 0; t < 2; ++t) {
       for (int st = 0; st < 2; ++st) {
-        mbar_init(&bars[B_KHFULL + 2 * t + st], kFusionThreads);
+        mbar_init(&bars[B_KHFULL + 2 * t + st], kFusionThreads / kArrive);
         mbar_init(&bars[B_KHEMPTY + 2 * t + st], 1);
       }
       mbar_init(&bars[B_SFULL + t], 1);
-      mbar_init(&bars[B_PFULL + t], 256);
+      mbar_init(&bars[B_PFULL + t], kSoftmaxThreads / kArrive);
       mbar_init(&bars[B_OFULL + t], 1);
     }
     fence_mbar_init();
@@ -354,16 +391,19 @@ __global__ void __launch_bounds__(threads_of<DISTR>(), 1)
     qhat_prologue<C, D, G, HB>(args, bars, sQst, sA, sKh, perm_s, bh, qt0, nkt_t[1] > 0 ? 2 : 1,
                                (int)threadIdx.x - 128, trace);
 
-  // Register split (distr, 512 threads at 128 registers): the TMA/MMA warpgroup gives 64 of its
-  // registers to the softmax warpgroups (128*64 + 256*160 + 128*128 = 512*128; an .inc that
-  // exceeds what the .dec released would block forever). The exact kernel (384 threads at 168)
-  // needs no split. Each setmaxnreg sits at the head of its warpgroup's branch so ptxas budgets
-  // each region separately.
+  // Register split (SPLIT = 2 only; distr, 512 threads at 128 registers): the TMA/MMA warpgroup
+  // gives 64 of its registers to the softmax warpgroups (128*64 + 256*160 + 128*128 = 512*128; an
+  // .inc that exceeds what the .dec released would block forever). The exact kernel (384 threads at
+  // 168) needs no split. With SPLIT = 4 every thread holds 32 scores and the launch-time budget
+  // (80 registers at 768 threads, 96 at 640) suffices. Each setmaxnreg sits at the head of its
+  // warpgroup's branch so ptxas budgets each region separately.
   if (warp < 4) {
-  if (DISTR)
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 48;");
-  else
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
+  if constexpr (kSplit == 2) {
+    if (DISTR)
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 48;");
+    else
+      asm volatile("setmaxnreg.dec.sync.aligned.u32 88;");
+  }
   if (warp == 0) {
     // ------------------------------------------------------------------ TMA producer
     if (lane == 0) {
@@ -475,69 +515,79 @@ __global__ void __launch_bounds__(threads_of<DISTR>(), 1)
       release_v(nk - 1);
     }
   }  // warp 3 idle
-  } else if (warp < 12) {
-    if (DISTR)
-      asm volatile("setmaxnreg.inc.sync.aligned.u32 160;");
-    // ------------------------------------------------------------------ softmax (warps 4..11)
-    // All 8 softmax warps work on ONE Q tile at a time, alternating tiles (t = 0, 1, 0, 1, ...)
-    // in the MMA's issue order. Warps w and w+4 own the same 32 TMEM lanes (rows) and split the
-    // 128 key columns: half = (w - 4) / 4 takes columns [64*half, 64*half + 64). The row max is
-    // combined through shared memory with a 64-thread named barrier per warp pair; the running
-    // max m is therefore identical in both halves, so each half keeps its own partial row sum and
-    // rescales its own half of O's columns; the halves' sums are combined once, at the end.
+  } else if (warp < 4 + kSoftmaxWarps) {
+    if constexpr (kSplit == 2) {
+      if (DISTR) asm volatile("setmaxnreg.inc.sync.aligned.u32 160;");
+    }
+    // ------------------------------------------------------------------ softmax (warps 4..4+4*SPLIT)
+    // All softmax warps work on ONE Q tile at a time, alternating tiles (t = 0, 1, 0, 1, ...) in
+    // the MMA's issue order. The SPLIT warps w = 4 + quad + 4*part own the same 32 TMEM lanes
+    // (rows) and split the 128 key columns: part takes columns [CW*part, CW*part + CW). The row max
+    // is combined through shared memory with a (32*SPLIT)-thread named barrier per quad; the
+    // running max m is therefore identical in every part, so each part keeps its own partial row
+    // sum and rescales its own D/SPLIT columns of O; the parts' sums are combined once, at the end.
     // While these warps run tile t's exp phase the tensor core computes the other tile.
-    const int half = (warp - 4) >> 2;
+    constexpr int CW = kCW;
+    const int part = (warp - 4) >> 2;
     const int quad = warp & 3;
-    constexpr int OC = D / 2 >= 32 ? 32 : 16;  // O columns per TMEM load in the rescale / epilogue
+    constexpr int DP = D / kSplit;             // O columns per part
+    constexpr int OC = DP >= 32 ? 32 : DP;     // O columns per TMEM load in the rescale / epilogue
     const int row = quad * 32 + lane;
     const uint32_t lane_base = (uint32_t)(quad * 32) << 16;
-    float* xmax = reinterpret_cast<float*>(bars + B_COUNT);  // max [2 parity][2 t][2 half][128], sums [2 t][2 half][128]
+    // max [2 parity][2 t][SPLIT][128], sums [2 t][SPLIT][128]
+    float* xmax = reinterpret_cast<float*>(bars + B_COUNT);
+    float* xsum = xmax + 4 * kSplit * 128;
     const float sl2 = args.scale_log2;
     float m[2] = {-INFINITY, -INFINITY};  // running max per tile (scaled log2; stale by <= 8)
-    float l[2] = {0.0f, 0.0f};            // this half's partial row sums
-    auto pair_sync = [&]() {  // warps quad+4 and quad+8 (same rows, both halves)
-      asm volatile("bar.sync %0, 64;" ::"r"(1 + quad) : "memory");
+    float l[2] = {0.0f, 0.0f};            // this part's partial row sums
+    auto quad_sync = [&]() {  // the SPLIT warps of this quad (same rows, all parts)
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + quad), "n"(32 * kSplit) : "memory");
     };
     for (int i = 0; i < nk; ++i) {
 #pragma unroll
       for (int t = 0; t < 2; ++t) {
         if (i >= nkt_t[t]) continue;
-        const uint32_t tS = tmem + lane_base + kColS + 128u * t + 64u * half;
-        const uint32_t tO = tmem + lane_base + (uint32_t)(t * D) + (uint32_t)(half * (D / 2));
+        const uint32_t tS = tmem + lane_base + kColS + 128u * t + (uint32_t)(CW * part);
+        const uint32_t tO = tmem + lane_base + (uint32_t)(t * D) + (uint32_t)(part * DP);
         const int q0 = (qt0 + t) * BM;
         const int q_row = q0 + row;
-        DA_TRACE(13 + t, i, row == 0 && half == 0);
+        DA_TRACE(13 + t, i, row == 0 && part == 0);
         mbar_wait(&bars[B_SFULL + t], i & 1);
-        DA_TRACE(3 * t, i, row == 0 && half == 0);
+        DA_TRACE(3 * t, i, row == 0 && part == 0);
         tc_fence_after();
-        uint32_t sr[64];
-        tmem_ld32(tS, *reinterpret_cast<uint32_t(*)[32]>(&sr[0]));
-        tmem_ld32(tS + 32u, *reinterpret_cast<uint32_t(*)[32]>(&sr[32]));
-        tmem_ld_wait();
-        float sv[64];
+        uint32_t sr[CW];
 #pragma unroll
-        for (int e = 0; e < 64; ++e) sv[e] = __uint_as_float(sr[e]);
-        const int kbase = i * BN + 64 * half;
-        if (kbase + 64 > args.N || (args.causal && kbase + 63 > q0)) {
+        for (int c = 0; c < CW / 32; ++c) tmem_ld32(tS + 32u * c, *reinterpret_cast<uint32_t(*)[32]>(&sr[32 * c]));
+        tmem_ld_wait();
+        float sv[CW];
+#pragma unroll
+        for (int e = 0; e < CW; ++e) sv[e] = __uint_as_float(sr[e]);
+        const int kbase = i * BN + CW * part;
+        if (kbase + CW > args.N || (args.causal && kbase + CW - 1 > q0)) {
           const int lim = args.causal ? min(args.N - 1, q_row) : args.N - 1;
 #pragma unroll
-          for (int e = 0; e < 64; ++e)
+          for (int e = 0; e < CW; ++e)
             if (kbase + e > lim) sv[e] = -INFINITY;
         }
-        // Row max over this half: 8 independent FMNMX3 chains; then combine the two halves.
+        // Row max over this part: 8 independent FMNMX3 chains; then combine the parts.
         float mx8[8];
 #pragma unroll
-        for (int j = 0; j < 8; ++j) mx8[j] = max3(sv[j], sv[8 + j], sv[56 + j]);
+        for (int j = 0; j < 8; ++j) mx8[j] = max3(sv[j], sv[8 + j], sv[16 + j]);
 #pragma unroll
-        for (int e = 16; e < 56; e += 16)
+        for (int e = 24; e + 16 <= CW; e += 16)
 #pragma unroll
           for (int j = 0; j < 8; ++j) mx8[j] = max3(mx8[j], sv[e + j], sv[e + 8 + j]);
+        static_assert((CW - 24) % 16 == 8, "max tree tail");
+#pragma unroll
+        for (int j = 0; j < 8; ++j) mx8[j] = fmaxf(mx8[j], sv[CW - 8 + j]);
         float mx = max3(max3(mx8[0], mx8[1], mx8[2]), max3(mx8[3], mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]));
-        xmax[((i & 1) * 4 + t * 2 + half) * 128 + row] = mx;
-        pair_sync();
-        mx = fmaxf(mx, xmax[((i & 1) * 4 + t * 2 + (half ^ 1)) * 128 + row]);
+        float* xm = xmax + ((i & 1) * 2 + t) * kSplit * 128 + row;
+        xm[part * 128] = mx;
+        quad_sync();
+#pragma unroll
+        for (int o = 1; o < kSplit; ++o) mx = fmaxf(mx, xm[((part + o) % kSplit) * 128]);
         const float mnew = fmaxf(m[t], mx * sl2);
-        DA_TRACE(3 * t + 1, i, row == 0 && half == 0);
+        DA_TRACE(3 * t + 1, i, row == 0 && part == 0);
         if (i == 0) {
           m[t] = mnew;
         } else {
@@ -546,7 +596,7 @@ __global__ void __launch_bounds__(threads_of<DISTR>(), 1)
           if (__any_sync(0xffffffffu, need)) {
             const float f = need ? ex2(m[t] - mnew) : 1.0f;
 #pragma unroll
-            for (int c = 0; c < D / 2 / OC; ++c) {
+            for (int c = 0; c < DP / OC; ++c) {
               uint32_t r[OC];
               tmem_ldn<OC>(tO + (uint32_t)(OC * c), r);
               tmem_ld_wait();
@@ -565,49 +615,56 @@ __global__ void __launch_bounds__(threads_of<DISTR>(), 1)
         const float2 sl2x2 = make_float2(sl2, sl2), nm2 = make_float2(-m[t], -m[t]);
         float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
                          make_float2(0.f, 0.f)};
-        uint32_t pr[32];
+        uint32_t pr[CW / 2];
 #pragma unroll
-        for (int e = 0; e < 32; ++e) {
+        for (int e = 0; e < CW / 2; ++e) {
           const float2 x = fma2(make_float2(sv[2 * e], sv[2 * e + 1]), sl2x2, nm2);
           float2 p;
-          if ((e & 7) >= 8 - EMU)
+          // polynomial pairs: the last EMU of every 8, or (DA_EMU_SPREAD) spread evenly so the
+          // MUFU and FMA-pipe instructions interleave in each warp's stream
+          if (DA_EMU_SPREAD ? ((e * EMU) & 7) < EMU : (e & 7) >= 8 - EMU)
             p = exp2_poly2(x);
           else
             p = make_float2(ex2(x.x), ex2(x.y));
           acc[e & 3] = fadd2(acc[e & 3], p);
           pr[e] = pack_bf16x2(p.x, p.y);
-          // P of keys [64*half, 64*half + 64) -> columns [32*half, 32*half + 32) of S_t, stored
-          // in 8-column chunks as they complete so the TMEM writes drain under the remaining exps
-          if ((e & 7) == 7) tmem_st8(tmem + lane_base + kColS + 128u * t + 32u * half + (e - 7), &pr[e - 7]);
+          // P of keys [CW*part, CW*part + CW) -> columns [CW/2*part, CW/2*part + CW/2) of S_t,
+          // stored in 8-column chunks as they complete so the TMEM writes drain under the
+          // remaining exps
+          if ((e & 7) == 7)
+            tmem_st8(tmem + lane_base + kColS + 128u * t + (uint32_t)(CW / 2 * part) + (e - 7), &pr[e - 7]);
         }
-        DA_TRACE(16 + t, i, row == 0 && half == 0);
+        DA_TRACE(16 + t, i, row == 0 && part == 0);
         const float2 a = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
         l[t] += a.x + a.y;
         tmem_st_wait();
         tc_fence_before();
-        mbar_arrive(&bars[B_PFULL + t]);
-        DA_TRACE(3 * t + 2, i, row == 0 && half == 0);
+        warp_arrive(&bars[B_PFULL + t]);
+        DA_TRACE(3 * t + 2, i, row == 0 && part == 0);
       }
     }
-    // Epilogue: both halves' row sums, each half writes its d/2 output columns.
+    // Epilogue: all parts' row sums, each part writes its D/SPLIT output columns.
 #pragma unroll
     for (int t = 0; t < 2; ++t) {
       if (nkt_t[t] == 0) continue;
       const int q_row = (qt0 + t) * BM + row;
-      const uint32_t tO = tmem + lane_base + (uint32_t)(t * D) + (uint32_t)(half * (D / 2));
-      xmax[1024 + (t * 2 + half) * 128 + row] = l[t];
-      pair_sync();
-      const float lt = l[t] + xmax[1024 + (t * 2 + (half ^ 1)) * 128 + row];
+      const uint32_t tO = tmem + lane_base + (uint32_t)(t * D) + (uint32_t)(part * DP);
+      float* xs = xsum + t * kSplit * 128 + row;
+      xs[part * 128] = l[t];
+      quad_sync();
+      float lt = l[t];
+#pragma unroll
+      for (int o = 1; o < kSplit; ++o) lt += xs[((part + o) % kSplit) * 128];
       mbar_wait(&bars[B_OFULL + t], 0);
       tc_fence_after();
       const float inv = 1.0f / lt;
 #pragma unroll
-      for (int c = 0; c < D / 2 / OC; ++c) {
+      for (int c = 0; c < DP / OC; ++c) {
         uint32_t r[OC];
         tmem_ldn<OC>(tO + (uint32_t)(OC * c), r);
         tmem_ld_wait();
         if (q_row < args.N) {
-          const size_t off = ((size_t)bh * args.N + q_row) * D + half * (D / 2) + OC * c;
+          const size_t off = ((size_t)bh * args.N + q_row) * D + part * DP + OC * c;
           if (args.out_f32) {
             float4* o = reinterpret_cast<float4*>(static_cast<float*>(args.out) + off);
 #pragma unroll
@@ -625,7 +682,7 @@ __global__ void __launch_bounds__(threads_of<DISTR>(), 1)
           }
         }
       }
-      if (args.lse && q_row < args.N && half == 0)
+      if (args.lse && q_row < args.N && part == 0)
         args.lse[(size_t)bh * args.N + q_row] = (m[t] + log2f(lt)) * 0.69314718055994531f;
     }
   } else {
@@ -636,7 +693,7 @@ __global__ void __launch_bounds__(threads_of<DISTR>(), 1)
     // 16 lanes read one whole 256-byte K^T row (conflict-free); stores land in the UMMA
     // MN-major SWIZZLE_128B layout (chunk ^= row % 8, row % 8 == f/16 for every task).
     if (DISTR) {
-      const int f = threadIdx.x - 384;
+      const int f = threadIdx.x - (128 + kSoftmaxThreads);
       const int ch = f & 15, jb = f >> 4;
       constexpr int NT = C::DR / 8;  // tasks per thread per (tile, key tile)
       constexpr int DG = D / G;
@@ -669,6 +726,9 @@ __global__ void __launch_bounds__(threads_of<DISTR>(), 1)
           const int st = i % NKH;
           mbar_wait(&bars[B_KHEMPTY + 2 * t + st], ((i / NKH) & 1) ^ 1);
           uint8_t* kh = sKh + (t * NKH + st) * C::KH_BYTES + dbase;
+          if constexpr (DA_DIAG_NOFUSE) {
+            // diagnostic only (wrong results): no fusion work, to measure its interference
+          } else
 #pragma unroll
           for (int n = 0; n < NT; ++n) {
             uint32_t src[G];
@@ -706,10 +766,10 @@ __global__ void __launch_bounds__(threads_of<DISTR>(), 1)
             *reinterpret_cast<uint4*>(kh + n * 1024) = o;
           }
           fence_proxy_async_smem();
-          mbar_arrive(&bars[B_KHFULL + 2 * t + st]);
+          warp_arrive(&bars[B_KHFULL + 2 * t + st]);
           DA_TRACE(11 + t, i, f == 0);
         }
-        mbar_arrive(&bars[B_KEMPTY + s]);
+        warp_arrive(&bars[B_KEMPTY + s]);
       }
     }
   }

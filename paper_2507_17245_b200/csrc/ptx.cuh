@@ -175,6 +175,11 @@ DA_DEV void tmem_st16(uint32_t taddr, const uint32_t (&r)[16]) {
       "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]), "r"(r[14]), "r"(r[15])
       : "memory");
 }
+DA_DEV void tmem_ld8(uint32_t taddr, uint32_t (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+}
 DA_DEV void tmem_st8(uint32_t taddr, const uint32_t* r) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr), "r"(r[0]),
                "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
@@ -182,11 +187,15 @@ DA_DEV void tmem_st8(uint32_t taddr, const uint32_t* r) {
 }
 template <int NC>
 DA_DEV void tmem_ldn(uint32_t taddr, uint32_t (&r)[NC]) {
-  if constexpr (NC == 32) tmem_ld32(taddr, r); else tmem_ld16(taddr, r);
+  if constexpr (NC == 32) tmem_ld32(taddr, r);
+  else if constexpr (NC == 16) tmem_ld16(taddr, r);
+  else tmem_ld8(taddr, r);
 }
 template <int NC>
 DA_DEV void tmem_stn(uint32_t taddr, const uint32_t (&r)[NC]) {
-  if constexpr (NC == 32) tmem_st32(taddr, r); else tmem_st16(taddr, r);
+  if constexpr (NC == 32) tmem_st32(taddr, r);
+  else if constexpr (NC == 16) tmem_st16(taddr, r);
+  else tmem_st8(taddr, r);
 }
 DA_DEV void tmem_ld_wait() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 DA_DEV void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
