@@ -22,6 +22,13 @@ for r in data:
 print("total samples", samples)
 print("stall reasons:", ", ".join(f"{k[6:]} {v/samples*100:.1f}%" for k, v in tot.most_common(12)))
 print("samples by opcode:", ", ".join(f"{k} {v/samples*100:.1f}%" for k, v in by_op.most_common(15)))
+exc = [(num(r[ix["L1 Wavefronts Shared Excessive"]]), num(r[ix["L1 Wavefronts Shared"]]), r[ix["Address"]][-5:],
+        r[ix["Source"]].strip()[:60]) for r in data if len(r) >= len(hdr) and "L1 Wavefronts Shared Excessive" in ix]
+tw = sum(e[1] for e in exc); te = sum(e[0] for e in exc)
+if tw:
+    print(f"shared wavefronts {tw:.3e}, excessive (bank conflicts) {te:.3e} = {te / tw * 100:.1f}%; top excessive:")
+    for e, w, a, src in sorted(exc, reverse=True)[:12]:
+        if e > 0: print(f"  {e / te * 100:5.1f}% of excessive  {a} {src}  (wavefronts {w:.2e})")
 print("hottest instructions:")
 for s, a, src, st in sorted(ins, reverse=True)[:40]:
     print(f"  {s/samples*100:5.2f}% {a} {src:60s} {st}")
