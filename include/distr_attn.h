@@ -24,9 +24,11 @@
  *   - Thread safety: the projection cache and workspace pool are mutex-protected; concurrent
  *     calls that share a library-managed workspace on one device must use one stream.
  *
- * Supported envelope: d in {32, 64, 128}; block_l in {64, 128}; G* (group_size) in {1, 2, 4, 8} with
- * d % G* == 0 and the reduced width (128 / block_l) * d / G* in [16, 128]; any N >= 1 (ragged
- * tails handled); any B, H >= 1 with B*H, B*H_kv < 65536.
+ * Supported envelope: d in {32, 64, 128}; block_l in {64, 128, 256}; G* (group_size) in {1, 2, 4, 8}
+ * with d % G* == 0 and the reduced width max(1, 128 / block_l) * d / G* in [16, 128]; block_l = 256
+ * (one hash block = the 256 query rows one CTA owns, so both of its 128-row tiles share one
+ * grouping and one fused K̂ per key tile; P:306's "Q block" at the B200 CTA granularity) takes
+ * G* in {2, 4}; any N >= 1 (ragged tails handled); any B, H >= 1 with B*H, B*H_kv < 65536.
  */
 #ifndef DISTR_ATTN_H
 #define DISTR_ATTN_H
@@ -155,7 +157,7 @@ typedef struct da_plan {
   int tile_m;            /* query rows per Q tile (UMMA M) */
   int tiles_per_cta;     /* Q tiles per CTA */
   int tile_n;            /* keys per K/V tile: m (UMMA N of S, K of PV) */
-  int s_width;           /* contraction width of S: d (exact) or (128 / block_l) * d / G* */
+  int s_width;           /* contraction width of S: d (exact) or max(1, 128 / block_l) * d / G* */
   int kv_stages;         /* K (or K^T) and V TMA ring depth */
   int khat_stages;       /* fused K̂^T buffers per Q tile (distr) */
   int threads;           /* threads per CTA */

@@ -121,6 +121,7 @@ int get_pool(std::map<int, Pool>& pools, int dev, size_t need, void** out) {
 // ---------------------------------------------------------------------------- plan
 struct Plan {
   int B, H, Hkv, N, d, l, G, HB, DR, nqb, nqt, nkt, N_pad, f32, causal;
+  int KHB;  // attention-kernel HB: 128/block_l, or 0 for block_l = 256 (one grouping per CTA)
   int pair_off, pair_stride;  // Q-tile-pair shard (stride 1 = all pairs)
   float scale;
   size_t off_perm, off_qhat, off_kt, off_qc, off_kc, off_vc, total;
@@ -140,18 +141,21 @@ int validate(const da_params* p, bool distr, Plan* P) {
     return fail(DA_ERR_INVALID, "B*H too large");
   if (p->d != 32 && p->d != 64 && p->d != 128)
     return fail(DA_ERR_PRECONDITION, "d=%d unsupported (32|64|128)", p->d);
-  if (p->block_l != 64 && p->block_l != 128)
-    return fail(DA_ERR_PRECONDITION, "block_l=%d unsupported (64|128)", p->block_l);
+  if (p->block_l != 64 && p->block_l != 128 && p->block_l != 256)
+    return fail(DA_ERR_PRECONDITION, "block_l=%d unsupported (64|128|256)", p->block_l);
   const int G = distr ? p->group_size : 1;
   if (distr) {
     if (G <= 0) return fail(DA_ERR_INVALID, "group_size=%d", G);
     if (p->d % G) return fail(DA_ERR_PRECONDITION, "d %% G* != 0 (d=%d, G*=%d)", p->d, G);
     if (G != 1 && G != 2 && G != 4 && G != 8) return fail(DA_ERR_PRECONDITION, "G*=%d unsupported (1|2|4|8)", G);
     if (p->d / G < 16) return fail(DA_ERR_PRECONDITION, "d/G* = %d < 16", p->d / G);
+    if (p->block_l == 256 && G != 2 && G != 4)
+      return fail(DA_ERR_PRECONDITION, "block_l=256 supports G* in {2,4} (got %d)", G);
   }
   Plan& q = *P;
   q.B = p->B; q.H = p->H; q.Hkv = p->H_kv; q.N = p->N; q.d = p->d; q.l = p->block_l; q.G = G;
-  q.HB = 128 / p->block_l;
+  q.HB = p->block_l >= 128 ? 1 : 128 / p->block_l;
+  q.KHB = p->block_l == 256 ? 0 : q.HB;
   q.DR = q.HB * q.d / G;
   if (distr && (q.DR > 128 || q.DR < 16))
     return fail(DA_ERR_PRECONDITION, "reduced width (128/block_l)*d/G* = %d outside [16,128]", q.DR);
@@ -349,7 +353,7 @@ int forward(const void* q, const void* k, const void* v, void* out, const da_par
   aa.lse = p->lse;
   aa.trace = g_trace;
   g_trace = nullptr;
-  da::AttnLaunch L{P.d, P.G, P.HB, distr ? 1 : 0, (int)BH, &tmA, &tmK, &tmV, default_emu(P, distr)};
+  da::AttnLaunch L{P.d, P.G, distr ? P.KHB : 1, distr ? 1 : 0, (int)BH, &tmA, &tmK, &tmV, default_emu(P, distr)};
   record_ev(1, st);
   DA_CUDA(da::launch_attn(L, aa, st));
   record_ev(2, st);
@@ -687,7 +691,7 @@ int distr_attn_plan(int N, int d, int block_l, int group_size, int distr, da_pla
   Plan P;
   if (int s = validate(&p, distr != 0, &P)) return s;
   da::AttnConfig c;
-  if (!da::attn_config(P.d, P.G, P.HB, distr ? 1 : 0, &c))
+  if (!da::attn_config(P.d, P.G, distr ? P.KHB : 1, distr ? 1 : 0, &c))
     return fail(DA_ERR_PRECONDITION, "no kernel for d=%d G*=%d block_l=%d", P.d, P.G, P.l);
   *out = da_plan{};
   out->tile_m = 128;
@@ -706,7 +710,9 @@ int distr_attn_plan(int N, int d, int block_l, int group_size, int distr, da_pla
   const double m = out->tile_n;
   out->mma_clk_per_tile = 2.0 * 128 * m * (c.dr + P.d) / 8192.0;
   out->exp_clk_per_tile = 128.0 * m / 16.0;
-  out->fusion_smem_bytes_per_tile = distr ? (double)P.d * m * 2 + (double)c.dr * m * 2 : 0.0;
+  // block_l = 256: one K̂ per key tile serves both Q tiles of the CTA
+  out->fusion_smem_bytes_per_tile =
+      distr ? ((double)P.d * m * 2 + (double)c.dr * m * 2) / (P.KHB == 0 ? 2.0 : 1.0) : 0.0;
   const double Nd = (double)P.N * P.d, l = P.l;
   out->hbm_bytes_paper = 2.0 * ((double)P.N / l) * (l * P.d + 2.0 * Nd + l * P.d);
   out->hbm_bytes_b200 = 2.0 * 4.0 * Nd + (distr ? 2.0 * 2.0 * Nd : 0.0);

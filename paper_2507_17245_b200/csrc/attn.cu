@@ -81,10 +81,15 @@ constexpr uint32_t kTmemCols = 512;
 constexpr uint32_t kColS = 256;  // S_t at kColS + 128*t
 constexpr int kSmemMax = 232448 - 1024;
 
+// HB = hash blocks per 128-row Q tile: 2 (block_l = 64), 1 (block_l = 128), or 0 = one hash block
+// spanning both Q tiles of the CTA (block_l = 256): one grouping, one K̂ per key tile for both.
 template <int D, bool DISTR, int G, int HB>
 struct Cfg {
-  // contraction width of S: block-wise distr HB*d/G*; exact d (G = 1); global grouping d/G*
-  static constexpr int DR = DISTR ? HB * D / G : D / G;
+  static constexpr bool SHARED = DISTR && HB == 0;
+  static constexpr int HBE = HB == 0 ? 1 : HB;   // hash blocks stacked in one tile's Q̂
+  static constexpr int NKT = SHARED ? 1 : 2;     // K̂ buffer sets (one per Q tile, or one shared)
+  // contraction width of S: block-wise distr HBE*d/G*; exact d (G = 1); global grouping d/G*
+  static constexpr int DR = DISTR ? HBE * D / G : D / G;
   static constexpr int A_COLS = DR;
   static constexpr int A_SW = (A_COLS * 2 >= 128) ? 128 : A_COLS * 2;  // swizzle span (bytes)
   static constexpr int A_BOX_COLS = A_SW / 2;
@@ -94,9 +99,14 @@ struct Cfg {
   static constexpr int K_BYTES = BN * (DISTR ? D : DR) * 2;  // K^T tile (distr), K / K̂ tile (exact/global)
   static constexpr int V_BYTES = BN * D * 2;
   static constexpr int KH_BYTES = DISTR ? DR * BN * 2 : 0;
+  // the K̂ region doubles as the prologue's scratch: projection [l][16] fp32, then keys and parts
+  static constexpr int PROJ_BYTES = (SHARED ? 256 : 128) * 16 * 4;
+  static constexpr int kh_region(int nkh) {
+    return DISTR ? (NKT * nkh * KH_BYTES > PROJ_BYTES + 2048 ? NKT * nkh * KH_BYTES : PROJ_BYTES + 2048) : 0;
+  }
   static constexpr int al(int x) { return (x + 1023) / 1024 * 1024; }
   static constexpr int bytes(int ns, int nkh) {
-    return al(2 * A_BYTES) + ns * (K_BYTES + V_BYTES) + 2 * nkh * KH_BYTES + 1024 + 256 + kXchBytes;
+    return al(2 * A_BYTES) + ns * (K_BYTES + V_BYTES) + kh_region(nkh) + 1024 + 256 + kXchBytes;
   }
   // Deepest K/V ring (NS) and K̂ ring (NKH) that fit the 227 KB of shared memory.
   static constexpr int NKH = !DISTR ? 0 : (bytes(2, 2) <= kSmemMax ? 2 : 1);
@@ -105,7 +115,7 @@ struct Cfg {
   static constexpr int OFF_K = al(2 * A_BYTES);
   static constexpr int OFF_V = OFF_K + NS * K_BYTES;
   static constexpr int OFF_KH = OFF_V + NS * V_BYTES;
-  static constexpr int OFF_PERM = OFF_KH + 2 * NKH * KH_BYTES;
+  static constexpr int OFF_PERM = OFF_KH + kh_region(NKH);
   static constexpr int OFF_BAR = OFF_PERM + 2 * 2 * 128;
   static constexpr int SMEM = OFF_BAR + 256 + kXchBytes + 1024;  // barriers, row-max/sum exchange, align slack
   static constexpr uint32_t A_LAYOUT = A_SW == 128 ? kSw128 : (A_SW == 64 ? kSw64 : kSw32);
@@ -179,7 +189,7 @@ DA_DEV void qhat_prologue(const AttnArgs& args, uint64_t* bars, const uint8_t* s
   constexpr int DG = D / G;
   const int L = args.block_l;
   float* proj_t = reinterpret_cast<float*>(scratch);           // [l][16]
-  uint32_t* key_s = reinterpret_cast<uint32_t*>(scratch + 8192);  // [2][HB][D] keys + [2][HB][D][2] u8 parts
+  uint32_t* key_s = reinterpret_cast<uint32_t*>(scratch + C::PROJ_BYTES);  // [2][HB][D] keys, then u8 parts
   auto wsync = [] { asm volatile("bar.sync 5, %0;" ::"n"(kWorkers) : "memory"); };
   // byte offset of staged Q(t, r, c): box c / RB, RB*2-byte rows, SWIZZLE_{RB*2}B
   auto q_off = [&](int t, int r, int c) -> uint32_t {
@@ -193,49 +203,64 @@ DA_DEV void qhat_prologue(const AttnArgs& args, uint64_t* bars, const uint8_t* s
   wsync();
   PT(1)
   if (hash) {
-    // Projection: unit = (tile, hash block, column pair, half of the 16 projection rows): per row
-    // one 4-byte load of the two columns, two 16-byte (broadcast) projection loads, 8 FFMA2.
-    // The halves' 8-bit patterns are OR-ed through shared memory.
-    const int nunits = ntile * HB * D;
-    for (int u2 = ht; u2 < nunits; u2 += NW) {  // u2 = ((tile, hb, column pair) << 1) | k-half
-      const int kh = u2 & 1, cp = u2 >> 1;       // cp indexes (t, hb, c/2)
-      const int t = cp / (HB * D / 2), hb = (cp / (D / 2)) % HB, c = (cp % (D / 2)) * 2;
+    // Projection: unit = (tile, hash block, column pair, group of KG of the 16 projection rows):
+    // per row one 4-byte load of the two columns, KG/4 16-byte (broadcast) projection loads, KG
+    // FFMA2. KG = 8 for the per-tile blocks; the 256-row SHARED block has half / a quarter as many
+    // blocks, so it splits the projection rows finer (KG = 4 at d = 128, 2 below) to keep the
+    // chains of all worker threads busy. The groups' KG-bit patterns are OR-ed through smem.
+    constexpr int KG = !C::SHARED ? 8 : (D == 128 ? 4 : 2);
+    constexpr int NKG = 16 / KG;
+    const int nunits = (C::SHARED ? 1 : ntile * HB) * (D / 2) * NKG;  // (hash block, column pair, group)
+    uint8_t* parts = reinterpret_cast<uint8_t*>(key_s + 2 * C::HBE * D);  // [block, column][NKG]
+    for (int u2 = ht; u2 < nunits; u2 += NW) {
+      const int kg = u2 % NKG, cp = u2 / NKG;    // cp indexes (t, hb, c/2)
+      const int t = cp / (C::HBE * D / 2), hb = (cp / (D / 2)) % C::HBE, c = (cp % (D / 2)) * 2;
       const int row0 = (qt0 + t) * BM + hb * L;  // first global row of this hash block
       const int rows = max(0, min(L, args.N - row0));
-      float2 ya[4], yb[4];  // column c / c+1, projection rows 8kh .. 8kh+7
+      float2 ya[KG / 2], yb[KG / 2];  // column c / c+1, projection rows KG*kg .. KG*kg + KG-1
 #pragma unroll
-      for (int m = 0; m < 4; ++m) ya[m] = yb[m] = make_float2(0.0f, 0.0f);
-      const float* pr = proj_t + 8 * kh;
+      for (int m = 0; m < KG / 2; ++m) ya[m] = yb[m] = make_float2(0.0f, 0.0f);
+      const float* pr = proj_t + KG * kg;
 #pragma unroll kHashUnroll
-      for (int r = 0; r < rows; ++r) {
-        const uint32_t q2 = *reinterpret_cast<const uint32_t*>(sQ + q_off(t, hb * L + r, c));
+      for (int r = 0; r < rows; ++r) {  // ascending rows: the R6 fp32 fma chain
+        const uint32_t q2 = *reinterpret_cast<const uint32_t*>(
+            sQ + (C::SHARED ? q_off(r >> 7, r & (BM - 1), c) : q_off(t, hb * L + r, c)));
         const float qa = __uint_as_float(q2 << 16), qb = __uint_as_float(q2 & 0xFFFF0000u);
-        const float4 p0 = *reinterpret_cast<const float4*>(pr + r * 16);
-        const float4 p1 = *reinterpret_cast<const float4*>(pr + r * 16 + 4);
-        const float2 pk[4] = {make_float2(p0.x, p0.y), make_float2(p0.z, p0.w), make_float2(p1.x, p1.y),
-                              make_float2(p1.z, p1.w)};
+        float2 pk[KG / 2];
+        if constexpr (KG == 2) {
+          pk[0] = *reinterpret_cast<const float2*>(pr + r * 16);
+        } else {
 #pragma unroll
-        for (int m = 0; m < 4; ++m) {
+          for (int v4 = 0; v4 < KG / 4; ++v4) {
+            const float4 p4 = *reinterpret_cast<const float4*>(pr + r * 16 + 4 * v4);
+            pk[2 * v4] = make_float2(p4.x, p4.y);
+            pk[2 * v4 + 1] = make_float2(p4.z, p4.w);
+          }
+        }
+#pragma unroll
+        for (int m = 0; m < KG / 2; ++m) {
           ya[m] = fma2(pk[m], make_float2(qa, qa), ya[m]);
           yb[m] = fma2(pk[m], make_float2(qb, qb), yb[m]);
         }
       }
       uint32_t ba = 0, bb = 0;
 #pragma unroll
-      for (int m = 0; m < 4; ++m) {
+      for (int m = 0; m < KG / 2; ++m) {
         ba |= (ya[m].x > 0.0f ? 1u : 0u) << (2 * m) | (ya[m].y > 0.0f ? 1u : 0u) << (2 * m + 1);
         bb |= (yb[m].x > 0.0f ? 1u : 0u) << (2 * m) | (yb[m].y > 0.0f ? 1u : 0u) << (2 * m + 1);
       }
-      uint8_t* parts = reinterpret_cast<uint8_t*>(key_s + 2 * HB * D);  // [unit][2 halves]
-      const int u = (t * HB + hb) * D + c;
-      parts[2 * u + kh] = (uint8_t)ba;
-      parts[2 * (u + 1) + kh] = (uint8_t)bb;
+      const int u = (t * C::HBE + hb) * D + c;
+      parts[u * NKG + kg] = (uint8_t)ba;
+      parts[(u + 1) * NKG + kg] = (uint8_t)bb;
     }
     wsync();
-    for (int u = ht; u < nunits; u += NW) {
-      const uint32_t pattern = reinterpret_cast<const uint16_t*>(key_s + 2 * HB * D)[u];  // halves lo | hi << 8
+    const int ncols = (C::SHARED ? 1 : ntile * HB) * D;  // (hash block, column) units
+    for (int u = ht; u < ncols; u += NW) {
+      uint32_t pattern = 0;
+#pragma unroll
+      for (int g = 0; g < NKG; ++g) pattern |= (uint32_t)parts[u * NKG + g] << (KG * g);
       const uint32_t bucket = inverse_gray16(pattern);
-      const int t = u / (HB * D), hb = (u / D) % HB, c = u % D;
+      const int t = u / (C::HBE * D), hb = (u / D) % C::HBE, c = u % D;
       key_s[u] = (bucket << 8) | (uint32_t)c;
       const int row0 = (qt0 + t) * BM + hb * L;
       if (args.bucket_out && row0 < args.N)
@@ -243,7 +268,7 @@ DA_DEV void qhat_prologue(const AttnArgs& args, uint64_t* bars, const uint8_t* s
     }
     wsync();
     PT(2)
-    for (int u = ht; u < nunits; u += NW) {
+    for (int u = ht; u < ncols; u += NW) {
       const uint4* ks = reinterpret_cast<const uint4*>(key_s + (u / D) * D);
       const uint32_t mine = key_s[u];
       int rank = 0;
@@ -254,13 +279,14 @@ DA_DEV void qhat_prologue(const AttnArgs& args, uint64_t* bars, const uint8_t* s
       }
       const int c = u % D;
       perm_s[(u / D) * D + rank] = (uint8_t)c;
-      const int qb = ((qt0 + u / (HB * D)) * BM) / L + (u / D) % HB;
+      if (C::SHARED) perm_s[D + rank] = (uint8_t)c;  // tile 1 uses the same grouping
+      const int qb = ((qt0 + u / (C::HBE * D)) * BM) / L + (u / D) % C::HBE;
       if (args.perm_out && qb < args.nqb)
         args.perm_out[((size_t)bh * args.nqb + qb) * D + rank] = (uint8_t)c;
     }
   } else {
-    for (int u = ht; u < ntile * HB * D; u += NW) {
-      const int t = u / (HB * D), hb = (u / D) % HB, c = u % D;
+    for (int u = ht; u < ntile * C::HBE * D; u += NW) {
+      const int t = u / (C::HBE * D), hb = (u / D) % C::HBE, c = u % D;
       const int qb = (qt0 + t) * BM / L + hb;
       perm_s[u] = (qb < args.nqb) ? args.perm[((size_t)bh * args.nqb + qb) * D + c] : (uint8_t)c;
     }
@@ -282,7 +308,7 @@ DA_DEV void qhat_prologue(const AttnArgs& args, uint64_t* bars, const uint8_t* s
 #pragma unroll
       for (int e = 0; e < 8; ++e) {
         const int j = ch * 8 + e, hbj = j / DG, jj = j % DG;
-        src[hbr][e] = (HB == 2 && hbj != hbr) || (HB == 1 && hbr == 1) ? -1 : perm_s[(t * HB + hbj) * D + jj * G];
+        src[hbr][e] = (HB == 2 && hbj != hbr) || (HB != 2 && hbr == 1) ? -1 : perm_s[(t * C::HBE + hbj) * D + jj * G];
       }
     const int j0 = ch * 8;
     const uint32_t dcol = (uint32_t)((j0 / C::A_BOX_COLS) * C::A_BOX_BYTES + (j0 % C::A_BOX_COLS) * 2);
@@ -458,8 +484,9 @@ __global__ void __launch_bounds__(threads_of<DISTR>(), 1)
       const uint32_t a_base = smem_u32(sA);
       auto issue_s = [&](int t, int i) {
         const int s = i % NS;
+        const int tk = C::SHARED ? 0 : t;  // K̂ buffer set this tile reads
         if (DISTR)
-          mbar_wait(&bars[B_KHFULL + 2 * t + i % NKH], (i / NKH) & 1);
+          mbar_wait(&bars[B_KHFULL + 2 * tk + i % NKH], (i / NKH) & 1);
         else if (t == 0 || nkt_t[0] <= i)  // first consumer of K tile i waits for it
           mbar_wait(&bars[B_KFULL + s], (i / NS) & 1);
         tc_fence_after();
@@ -472,7 +499,7 @@ __global__ void __launch_bounds__(threads_of<DISTR>(), 1)
           uint64_t bdesc;
           if (DISTR) {
             // K̂^T as the MN-major B operand: 64-key blocks (LBO = DR*128 B), 8-row groups (SBO).
-            bdesc = make_sdesc(smem_u32(sKh + (t * NKH + i % NKH) * C::KH_BYTES) + kk * 2048, C::DR * 128, 1024,
+            bdesc = make_sdesc(smem_u32(sKh + (tk * NKH + i % NKH) * C::KH_BYTES) + kk * 2048, C::DR * 128, 1024,
                                kSw128);
           } else {
             bdesc = make_sdesc(smem_u32(sK + s * C::K_BYTES) + (kk / kpb) * C::A_BOX_BYTES + (kk % kpb) * 32, 16,
@@ -481,7 +508,9 @@ __global__ void __launch_bounds__(threads_of<DISTR>(), 1)
           mma_ss(d_s, adesc, bdesc, IDESC_S, kk > 0 ? 1u : 0u);
         }
         mma_commit(&bars[B_SFULL + t]);
-        if (DISTR) mma_commit(&bars[B_KHEMPTY + 2 * t + i % NKH]);
+        // K̂ stage free once its last reader has issued (SHARED: tile 1 if it uses key tile i; tile 1
+        // never uses fewer key tiles than tile 0)
+        if (DISTR && (!C::SHARED || t == 1 || i >= nkt_t[1])) mma_commit(&bars[B_KHEMPTY + 2 * tk + i % NKH]);
         DA_TRACE(6 + t, i, true);
       };
       auto issue_pv = [&](int t, int j) {
@@ -765,7 +794,7 @@ __global__ void __launch_bounds__(threads_of<DISTR>(), 1)
 #pragma unroll
           for (int g = 0; g < G; ++g) {
             const int e = n * G + g;
-            const uint32_t o = (uint32_t)perm_s[(t * HB + hb) * D + jj * G + g] * (BN * 2) + ch * 16;
+            const uint32_t o = (uint32_t)perm_s[(t * C::HBE + hb) * D + jj * G + g] * (BN * 2) + ch * 16;
             offs[t][e >> 1] |= o << (16 * (e & 1));
           }
         }
@@ -777,8 +806,8 @@ __global__ void __launch_bounds__(threads_of<DISTR>(), 1)
         DA_TRACE(10, i, f == 0);
         const uint8_t* kt = sK + s * C::K_BYTES;
 #pragma unroll
-        for (int t = 0; t < 2; ++t) {
-          if (i >= nkt_t[t]) continue;
+        for (int t = 0; t < C::NKT; ++t) {  // SHARED: one K̂ for both Q tiles (i < nk: someone uses it)
+          if (!C::SHARED && i >= nkt_t[t]) continue;
           const int st = i % NKH;
           mbar_wait(&bars[B_KHEMPTY + 2 * t + st], ((i / NKH) & 1) ^ 1);
           uint8_t* kh = sKh + (t * NKH + st) * C::KH_BYTES + dbase;
@@ -886,6 +915,11 @@ constexpr size_t smem_of() {
     if (d == 128 && G == 4 && HB == 2) MACRO(128, true, 4, 2);                      \
     if (d == 128 && G == 8 && HB == 1) MACRO(128, true, 8, 1);                      \
     if (d == 128 && G == 8 && HB == 2) MACRO(128, true, 8, 2);                      \
+    if (d == 32 && G == 2 && HB == 0) MACRO(32, true, 2, 0);                        \
+    if (d == 64 && G == 2 && HB == 0) MACRO(64, true, 2, 0);                        \
+    if (d == 64 && G == 4 && HB == 0) MACRO(64, true, 4, 0);                        \
+    if (d == 128 && G == 2 && HB == 0) MACRO(128, true, 2, 0);                      \
+    if (d == 128 && G == 4 && HB == 0) MACRO(128, true, 4, 0);                      \
   }
 
 size_t attn_smem_bytes(int d, int G, int HB, int distr) {

@@ -25,7 +25,7 @@ namespace da {
 namespace {
 
 constexpr int kThreads = 256;
-constexpr int kMaxL = 128;
+constexpr int kMaxL = 256;  // largest block_l (the staging below works in 128-row chunks)
 
 template <typename T>
 DA_DEV float load_f(const T* p);
@@ -60,14 +60,14 @@ constexpr int q_pitch() { return D + 16 / (int)sizeof(T); }
 template <typename T, int D>
 DA_DEV void hash_cta(const PrepArgs& a, int it, uint8_t* smem) {
   constexpr int QP = q_pitch<T, D>();
-  constexpr int QBYTES = kMaxL * QP * (int)sizeof(T);
+  const int QBYTES = a.block_l * QP * (int)sizeof(T);  // smem is sized for this launch's block_l
   const int bh = it / a.nqb, qb = it - bh * a.nqb;
   const int r0 = qb * a.block_l;
   const int rows = min(a.block_l, a.N - r0);
   const int lsh = ilog2(a.block_l);
   T* q_s = reinterpret_cast<T*>(smem);                                 // [rows][QP]
   float* proj_t = reinterpret_cast<float*>(smem + QBYTES);             // [r][16]
-  uint32_t* pat_s = reinterpret_cast<uint32_t*>(proj_t + kMaxL * 16);  // [NKG][D] = kThreads
+  uint32_t* pat_s = reinterpret_cast<uint32_t*>(proj_t + a.block_l * 16);  // [NKG][D] = kThreads
   uint32_t* key_s = pat_s + kThreads;                                  // [D]
   uint8_t* perm_s = reinterpret_cast<uint8_t*>(key_s + D);             // [D]
 
@@ -75,19 +75,20 @@ DA_DEV void hash_cta(const PrepArgs& a, int it, uint8_t* smem) {
   const T* qg = reinterpret_cast<const T*>(a.q) + ((size_t)bh * a.N + r0) * D;
   constexpr int VEC = 16 / sizeof(T);
   constexpr int VPR = D / VEC;  // vectors per row
-  {
-    // all loads of a thread in flight before the first shared store
-    constexpr int NIT = kMaxL * VPR / kThreads;
+  for (int rb = 0; rb < rows; rb += 128) {
+    // all loads of a thread in flight before the first shared store (128-row chunks)
+    constexpr int NIT = 128 * VPR / kThreads;
+    const int cr = min(128, rows - rb);
     uint4 v[NIT];
 #pragma unroll
     for (int u = 0; u < NIT; ++u) {
       const int i = threadIdx.x + u * kThreads;
-      if (i < rows * VPR) v[u] = reinterpret_cast<const uint4*>(qg)[i];
+      if (i < cr * VPR) v[u] = reinterpret_cast<const uint4*>(qg + (size_t)rb * D)[i];
     }
 #pragma unroll
     for (int u = 0; u < NIT; ++u) {
       const int i = threadIdx.x + u * kThreads;
-      if (i < rows * VPR) *reinterpret_cast<uint4*>(q_s + (i / VPR) * QP + (i % VPR) * VEC) = v[u];
+      if (i < cr * VPR) *reinterpret_cast<uint4*>(q_s + (rb + i / VPR) * QP + (i % VPR) * VEC) = v[u];
     }
   }
   for (int i = threadIdx.x; i < 16 * a.block_l; i += kThreads) {
@@ -253,9 +254,9 @@ __global__ void convert_kernel(const float* __restrict__ src, uint16_t* __restri
 }
 
 template <typename T, int D>
-size_t prep_smem_bytes() {
-  const size_t q = (size_t)kMaxL * q_pitch<T, D>() * sizeof(T);
-  const size_t hash = q + kMaxL * 16 * 4 + kThreads * 4 + D * 4 + D + 16;
+size_t prep_smem_bytes(int block_l) {  // block_l = 0: no hash CTAs in this launch
+  const size_t q = (size_t)block_l * q_pitch<T, D>() * sizeof(T);
+  const size_t hash = block_l ? q + block_l * 16 * 4 + kThreads * 4 + D * 4 + D + 16 : 0;
   const size_t kt = 64 * D * 2;
   return std::max(hash, kt);
 }
@@ -263,7 +264,7 @@ size_t prep_smem_bytes() {
 template <typename T, int D>
 cudaError_t launch_prep_t(const PrepArgs& a, cudaStream_t st) {
   const int grid = a.n_hash_ctas + a.n_kt_ctas;
-  const size_t smem = prep_smem_bytes<T, D>();
+  const size_t smem = prep_smem_bytes<T, D>(a.n_hash_ctas ? a.block_l : 0);
   cudaError_t e = cudaFuncSetAttribute(prep_kernel<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   prep_kernel<T, D><<<grid, kThreads, smem, st>>>(a);

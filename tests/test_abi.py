@@ -72,6 +72,8 @@ FAKE = ctypes.c_void_p(0x1000)
     (dict(block_l=32), 2), (dict(d=64, block_l=64, G=1), 0), (dict(d=128, block_l=64, G=1), 2),
     (dict(d=128, block_l=128, G=8), 0), (dict(d=128, block_l=64, G=8), 0), (dict(d=128, G=16), 2),
     (dict(d=32, block_l=128, G=2), 0), (dict(d=32, block_l=64, G=2), 0), (dict(d=32, G=4), 2),
+    (dict(d=128, block_l=256, G=2), 0), (dict(d=64, block_l=256, G=4), 0), (dict(d=32, block_l=256, G=2), 0),
+    (dict(d=128, block_l=256, G=1), 2), (dict(d=128, block_l=256, G=8), 2), (dict(block_l=512), 2),
 ])
 def test_validation_before_any_cuda(L, kw, status):
     p = params(**kw)

@@ -61,7 +61,7 @@ def run(c: Config, seed=0):
 
 
 @pytest.mark.parametrize("d,l,G", [(32, 128, 2), (64, 64, 2), (64, 128, 4), (128, 128, 1), (128, 128, 2),
-                                   (128, 64, 2), (128, 128, 8)])
+                                   (128, 64, 2), (128, 128, 8), (128, 256, 2), (64, 256, 4)])
 @pytest.mark.parametrize("causal", [False, True])
 def test_backward_parity(d, l, G, causal):
     res = run(cfg(d=d, block_l=l, group_size=G, causal=causal))

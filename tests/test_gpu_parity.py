@@ -121,7 +121,9 @@ def test_exact_parity_configs(name):
                                          (64, 128, 2), (64, 128, 4), (128, 128, 1),
                                          (128, 128, 2), (128, 128, 4), (128, 64, 2),
                                          (128, 64, 4), (128, 128, 8), (128, 64, 8), (32, 128, 1),
-                                         (32, 128, 2), (32, 64, 1), (32, 64, 2)])
+                                         (32, 128, 2), (32, 64, 1), (32, 64, 2),
+                                         (32, 256, 2), (64, 256, 2), (64, 256, 4), (128, 256, 2),
+                                         (128, 256, 4)])
 @pytest.mark.parametrize("causal", [False, True])
 def test_distr_parity_envelope(d, block_l, G, causal):
     # several Q/K tiles plus ragged tails, GQA (H=4 over H_kv=2)
@@ -215,7 +217,8 @@ def test_error_against_exact_is_reported_not_gated():
 # Sequences with more than 8 key tiles hash their Q blocks inside the attention CTA
 # (qhat_prologue); shorter ones in the prep launch. These cases keep the in-CTA path covered.
 @pytest.mark.parametrize("d,block_l,G", [(32, 128, 2), (64, 64, 2), (64, 128, 4), (128, 128, 2),
-                                         (128, 64, 2), (128, 128, 8), (128, 128, 1)])
+                                         (128, 64, 2), (128, 128, 8), (128, 128, 1), (32, 256, 2),
+                                         (64, 256, 4), (128, 256, 2), (128, 256, 4)])
 @pytest.mark.parametrize("causal", [False, True])
 def test_in_cta_hash_path_parity(d, block_l, G, causal):
     cfg = cfg_small(B=1, H=2, H_kv=1, N=1300, d=d, block_l=block_l, group_size=G, causal=causal)
@@ -233,4 +236,20 @@ def test_in_cta_hash_path_parity(d, block_l, G, causal):
     want = oracle_items(q, k, v, items, block_l=block_l, G=G, seed=13, causal=causal)
     got = gather_items(out, items, block_l)
     mx, mean = errors(got, want, valid_rows_mask(items, cfg.N, block_l, d))
+    assert mx <= MAX_ABS and mean <= MEAN_ABS, (mx, mean)
+
+
+# ------------------------------------------------------------------------------ block_l = 256
+# One hash block = the 256 query rows of one CTA (both 128-row tiles share the grouping and the
+# fused K̂). Bucket ids from the prep hash (fp32 + distr_attn_hash) and from the in-CTA prologue.
+@pytest.mark.parametrize("N", [1, 200, 256, 257, 700])
+def test_block256_hash_bit_exact(N):
+    cfg = cfg_small(B=1, H=3, H_kv=3, N=N, d=128, block_l=256, group_size=2)
+    check_hash(cfg)
+
+
+@pytest.mark.parametrize("causal", [False, True])
+def test_block256_fp32_inputs(causal):
+    cfg = cfg_small(B=1, H=2, H_kv=1, N=600, d=64, block_l=256, group_size=2, causal=causal, dtype="f32")
+    mx, mean, _ = run_and_compare(cfg)
     assert mx <= MAX_ABS and mean <= MEAN_ABS, (mx, mean)

@@ -4,7 +4,7 @@ Fig. 9, P:468-498, P:712-720).
 
     python tools/pareto.py [--steps K] > gpurun_out/pareto.json   (one JSON line per variant)
 
-Variants: block-wise (block_l in {64, 128}) and global grouping (one LSH per head over all N
+Variants: block-wise (block_l in {64, 128, 256}) and global grouping (one LSH per head over all N
 rows; "block_l": "global"). Error: DistrAttention output vs the exact kernel's output on
 the same bf16 inputs (both on the GPU; the exact kernel itself matches the fp64 oracle to
 ~2e-3), for i.i.d. N(0,1) inputs, column-clustered Q (the structure LSH grouping is designed
@@ -29,8 +29,9 @@ ap.add_argument("--rounds", type=int, default=3)
 args = ap.parse_args()
 L = _native.lib()
 
-VARIANTS = [(d, l, g) for d in (32, 64, 128) for l in (64, 128) for g in (1, 2, 4, 8)
-            if d % g == 0 and d // g >= 16 and (128 // l) * d // g in range(16, 129)]
+VARIANTS = [(d, l, g) for d in (32, 64, 128) for l in (64, 128, 256) for g in (1, 2, 4, 8)
+            if d % g == 0 and d // g >= 16 and max(1, 128 // l) * d // g in range(16, 129)
+            and (l != 256 or g in (2, 4))]
 # global grouping (one LSH over all N rows per head): block_l = 0 marks it
 VARIANTS += [(d, 0, g) for d in (32, 64, 128) for g in (2, 4, 8) if d // g >= 16]
 DISTS = ("normal", "clustered", "block_clustered")
@@ -65,7 +66,7 @@ def run(q, k, v, out, evs, l, g, exact):
 
 
 for d, l, g in VARIANTS:
-    rec = {"d": d, "block_l": l if l else "global", "G": g, "DR": (128 // (l or 128)) * d // g}
+    rec = {"d": d, "block_l": l if l else "global", "G": g, "DR": max(1, 128 // (l or 128)) * d // g}
     base = CONFIGS["C4"].with_(B=1, H=8, H_kv=8, N=4096, d=d, block_l=l or 128, group_size=g)
     for dist in DISTS:
         q, k, v = make_qkv(base, device="cuda", dist=dist)

@@ -17,6 +17,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--steps", type=int, default=10)
 ap.add_argument("--warmup", type=int, default=3)
 ap.add_argument("--only", default="", help="comma-separated case-name prefixes (default: all)")
+ap.add_argument("--block-l", type=int, default=0, help="override block_l of every case (e.g. 256)")
 args = ap.parse_args()
 L = _native.lib()
 cases = [("C1", CONFIGS["C1"]), ("C2", CONFIGS["C2"]), ("C3", CONFIGS["C3"])]
@@ -24,6 +25,8 @@ cases += [(f"C4 N={n} G*={g}", CONFIGS["C4"].with_(N=n, group_size=g)) for n in 
 cases += [("C5 1-GPU", CONFIGS["C5"])]
 if args.only:
     cases = [c for c in cases if any(c[0].startswith(p) for p in args.only.split(","))]
+if args.block_l:
+    cases = [(f"{n} l={args.block_l}", c.with_(block_l=args.block_l)) for n, c in cases]
 
 
 def timed(fn):
