@@ -77,3 +77,16 @@ def test_plan_rejects_unsupported(args, status):
     with pytest.raises(DistrAttnError) as e:
         da.distr_attn_plan(N, d, block_l=l, group_size=g)
     assert e.value.status == status
+
+
+@pytest.mark.parametrize("d,g", [(32, 2), (64, 2), (64, 4), (128, 2), (128, 4)])
+def test_plan_block256_shares_one_grouping_per_cta(d, g):
+    # block_l = 256 = the two Q tiles of one CTA: S width d/G* (no stacking), one fused K̂ per key
+    # tile for both tiles (half the fusion traffic of block_l = 128), within the smem budget
+    p = da.distr_attn_plan(16384, d, block_l=256, group_size=g)
+    q = da.distr_attn_plan(16384, d, block_l=128, group_size=g)
+    assert p["s_width"] == q["s_width"] == d // g
+    assert p["fusion_smem_bytes_per_tile"] == q["fusion_smem_bytes_per_tile"] / 2
+    assert p["smem_bytes"] <= 232448 and p["khat_stages"] >= 1
+    # the paper's I/O model prefers the larger block
+    assert p["hbm_bytes_paper"] < q["hbm_bytes_paper"]
