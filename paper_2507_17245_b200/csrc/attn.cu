@@ -839,11 +839,7 @@ __global__ void __launch_bounds__(threads_of<DISTR>(), 1)
                 const uint4 x = *reinterpret_cast<const uint4*>(kt + src[g]);
                 const uint32_t xv[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                  const float2 fv = unpack_bf16x2(xv[e]);
-                  acc[2 * e] += fv.x;
-                  acc[2 * e + 1] += fv.y;
-                }
+                for (int e = 0; e < 4; ++e) add_bf16x2_f32(xv[e], acc[2 * e], acc[2 * e + 1]);
               }
               o = make_uint4(pack_bf16x2(acc[0], acc[1]), pack_bf16x2(acc[2], acc[3]), pack_bf16x2(acc[4], acc[5]),
                              pack_bf16x2(acc[6], acc[7]));

@@ -273,6 +273,14 @@ DA_DEV float2 exp2_poly2(float2 x) {
   return make_float2(__uint_as_float(__float_as_uint(t.x) * 8388608u + __float_as_uint(p.x)),
                      __uint_as_float(__float_as_uint(t.y) * 8388608u + __float_as_uint(p.y)));
 }
+// acc + the two bf16 halves of w, each into its own fp32 accumulator, with fp32 RN adds
+// (`add.rn.f32.bf16`, SASS FHADD.BF16: the same result as unpacking to fp32 and adding).
+DA_DEV void add_bf16x2_f32(uint32_t w, float& acc_lo, float& acc_hi) {
+  unsigned short lo, hi;
+  asm("mov.b32 {%0, %1}, %2;" : "=h"(lo), "=h"(hi) : "r"(w));
+  asm("add.rn.f32.bf16 %0, %1, %0;" : "+f"(acc_lo) : "h"(lo));
+  asm("add.rn.f32.bf16 %0, %1, %0;" : "+f"(acc_hi) : "h"(hi));
+}
 DA_DEV uint32_t pack_bf16x2(float lo, float hi) {
   uint32_t r;
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
