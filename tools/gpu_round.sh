@@ -24,7 +24,8 @@ done
 timeout -s KILL 60 python tools/trace.py distr > $O/trace_distr.log 2>&1
 timeout -s KILL 60 python tools/trace.py exact > $O/trace_exact.log 2>&1
 timeout -s KILL 600 python tools/sweep.py > $O/sweep.json 2> $O/sweep.err
-timeout -s KILL 900 python tools/pareto.py > $O/pareto.json 2> $O/pareto.err
+timeout -s KILL 600 python tools/sweep.py --only "C4 N=16384,C4 N=32768,C4 N=65536,C5" --block-l 256 > $O/sweep_l256.json 2> $O/sweep_l256.err
+timeout -s KILL 1500 python tools/pareto.py > $O/pareto.json 2> $O/pareto.err
 timeout -s KILL 600 python tools/bench_bwd.py > $O/bwd.json 2> $O/bwd.err
 timeout -s KILL 600 ncu --set full --clock-control none --import-source on -k regex:"bwd_kv_kernel|bwd_q_kernel" -c 2 -o $O/prof_bwd -f python tools/bench_bwd.py > $O/ncu_full_bwd.log 2>&1
 python tools/ncu_summary.py $O/prof_bwd.ncu-rep $O/ncu_bwd > $O/ncu_summary_bwd.log 2>&1; rm -f $O/prof_bwd.ncu-rep
