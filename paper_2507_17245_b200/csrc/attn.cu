@@ -39,9 +39,6 @@ constexpr int kHashUnroll = DA_HASH_UNROLL;  // rows of the projection chain unr
 #ifndef DA_DIAG_NOFUSE
 #define DA_DIAG_NOFUSE 0
 #endif
-#ifndef DA_SPEC
-#define DA_SPEC 0
-#endif
 #ifndef DA_EMU_SPREAD
 #define DA_EMU_SPREAD 0
 #endif
@@ -53,14 +50,6 @@ constexpr int kArrive = DA_WARP_ARRIVE ? 32 : 1;  // threads per arrival
 // softmax warps, 128/SPLIT columns per thread).
 constexpr int kSplit = DA_SPLIT;
 static_assert(kSplit == 2 || kSplit == 4, "softmax split");
-// Speculative softmax (SPLIT = 2): from the second key tile on, the exps of a tile run against the
-// running max m before the tile's own max is known, so the second half of the S load drains under
-// the first half's exps and the row max exchange leaves the front of the tile; if the tile's max
-// exceeds m by more than the lazy-rescale margin (2^8) the tile is redone with the new max (the
-// result is then identical to the non-speculative order). P of each part is kept inside the part's
-// own S columns ([CW*part, CW*part + CW/2)) so a part never overwrites S the other part still loads.
-constexpr bool kSpec = DA_SPEC && kSplit == 2;
-constexpr int kPOff = kSpec ? 128 / kSplit : 64 / kSplit;  // TMEM column offset of part p's P: kPOff*p
 
 namespace da {
 namespace {
@@ -526,9 +515,7 @@ __global__ void __launch_bounds__(threads_of<DISTR>(), 1)
           // V as the MN-major B operand: RB-column blocks (LBO) of 8-key groups (SBO).
           const uint64_t vdesc = make_sdesc(v_base + kk * 16 * C::RB * 2, BN * C::RB * 2, 8 * C::RB * 2,
                                             C::RB == 64 ? kSw128 : kSw64);
-          // keys [16kk, 16kk+16) belong to part 16kk/CW, whose P starts at column kPOff*part
-          const uint32_t pcol = (uint32_t)(8 * kk + (16 * kk / kCW) * (kPOff - kCW / 2));
-          mma_ts(tmem + (uint32_t)(t * D), p_tmem + pcol, vdesc, IDESC_PV, (j > 0 || kk > 0) ? 1u : 0u);
+          mma_ts(tmem + (uint32_t)(t * D), p_tmem + kk * 8, vdesc, IDESC_PV, (j > 0 || kk > 0) ? 1u : 0u);
         }
         if (j == nkt_t[t] - 1) mma_commit(&bars[B_OFULL + t]);
       };
@@ -597,127 +584,84 @@ __global__ void __launch_bounds__(threads_of<DISTR>(), 1)
         mbar_wait(&bars[B_SFULL + t], i & 1);
         DA_TRACE(3 * t, i, row == 0 && part == 0);
         tc_fence_after();
+        uint32_t sr[CW];
+#pragma unroll
+        for (int c = 0; c < CW / 32; ++c) tmem_ld32(tS + 32u * c, *reinterpret_cast<uint32_t(*)[32]>(&sr[32 * c]));
+        tmem_ld_wait();
         float sv[CW];
+#pragma unroll
+        for (int e = 0; e < CW; ++e) sv[e] = __uint_as_float(sr[e]);
         const int kbase = i * BN + CW * part;
-        const bool masked = kbase + CW > args.N || (args.causal && kbase + CW - 1 > q0);
-        const int lim = args.causal ? min(args.N - 1, q_row) : args.N - 1;
-        // scores of columns [32c, 32c + 32) of this part, causal / ragged masked to -inf
-        auto take = [&](const uint32_t(&r)[32], int c) {
+        if (kbase + CW > args.N || (args.causal && kbase + CW - 1 > q0)) {
+          const int lim = args.causal ? min(args.N - 1, q_row) : args.N - 1;
 #pragma unroll
-          for (int e = 0; e < 32; ++e) sv[32 * c + e] = __uint_as_float(r[e]);
-          if (masked) {
+          for (int e = 0; e < CW; ++e)
+            if (kbase + e > lim) sv[e] = -INFINITY;
+        }
+        // Row max over this part: 8 independent FMNMX3 chains; then combine the parts.
+        float mx8[8];
 #pragma unroll
-            for (int e = 0; e < 32; ++e)
-              if (kbase + 32 * c + e > lim) sv[32 * c + e] = -INFINITY;
-          }
-        };
-        // row max of sv[e0, e0 + n): 8 independent FMNMX3 chains (n a multiple of 8, >= 24)
-        auto rmax = [&](int e0, int n) {
-          float mx8[8];
+        for (int j = 0; j < 8; ++j) mx8[j] = max3(sv[j], sv[8 + j], sv[16 + j]);
 #pragma unroll
-          for (int j = 0; j < 8; ++j) mx8[j] = max3(sv[e0 + j], sv[e0 + 8 + j], sv[e0 + 16 + j]);
+        for (int e = 24; e + 16 <= CW; e += 16)
 #pragma unroll
-          for (int e = 24; e + 16 <= n; e += 16)
+          for (int j = 0; j < 8; ++j) mx8[j] = max3(mx8[j], sv[e + j], sv[e + 8 + j]);
+        static_assert((CW - 24) % 16 == 8, "max tree tail");
 #pragma unroll
-            for (int j = 0; j < 8; ++j) mx8[j] = max3(mx8[j], sv[e0 + e + j], sv[e0 + e + 8 + j]);
+        for (int j = 0; j < 8; ++j) mx8[j] = fmaxf(mx8[j], sv[CW - 8 + j]);
+        float mx = max3(max3(mx8[0], mx8[1], mx8[2]), max3(mx8[3], mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]));
+        float* xm = xmax + ((i & 1) * 2 + t) * kSplit * 128 + row;
+        xm[part * 128] = mx;
+        quad_sync();
 #pragma unroll
-          for (int j = 0; j < 8; ++j) mx8[j] = fmaxf(mx8[j], sv[e0 + n - 8 + j]);
-          return max3(max3(mx8[0], mx8[1], mx8[2]), max3(mx8[3], mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]));
-        };
-        // combine the parts' maxima through shared memory
-        auto exchange = [&](float mx) {
-          float* xm = xmax + ((i & 1) * 2 + t) * kSplit * 128 + row;
-          xm[part * 128] = mx;
-          quad_sync();
-#pragma unroll
-          for (int o = 1; o < kSplit; ++o) mx = fmaxf(mx, xm[((part + o) % kSplit) * 128]);
-          return mx;
-        };
-        // lazy rescale: only when the running max grows by more than 2^8 (the normaliser uses the
-        // same stale max, so the result is exact); S_t(i) was committed after PV_t(i-1) was issued,
-        // so O_t holds sum_{<i} P V. Returns whether any lane of the warp rescaled.
-        auto rescale = [&](float mnew) {
-          const bool need = mnew > m[t] + 8.0f;
-          if (!__any_sync(0xffffffffu, need)) return false;
-          const float f = need ? ex2(m[t] - mnew) : 1.0f;
-#pragma unroll
-          for (int c = 0; c < DP / OC; ++c) {
-            uint32_t r[OC];
-            tmem_ldn<OC>(tO + (uint32_t)(OC * c), r);
-            tmem_ld_wait();
-#pragma unroll
-            for (int e = 0; e < OC; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * f);
-            tmem_stn<OC>(tO + (uint32_t)(OC * c), r);
-          }
-          if (need) {
-            l[t] *= f;
-            m[t] = mnew;
-          }
-          return true;
-        };
-        // p = 2^(s*scale*log2e - m) for pairs [e0, e1): FFMA2 for the affine part, EMU/8 of the
-        // pairs on the FMA pipe, the rest on MUFU; 4 independent FADD2 partial sums. P of keys
-        // [CW*part, CW*part + CW) -> columns [kPOff*part, kPOff*part + CW/2) of S_t, stored in
-        // 8-column chunks as they complete so the TMEM writes drain under the remaining exps.
-        float2 acc[4];
-        uint32_t pr[CW / 2];
-        auto exps = [&](int e0, int e1) {
-          const float2 sl2x2 = make_float2(sl2, sl2), nm2 = make_float2(-m[t], -m[t]);
-#pragma unroll
-          for (int e = 0; e < CW / 2; ++e) {
-            if (e < e0 || e >= e1) continue;
-            const float2 x = fma2(make_float2(sv[2 * e], sv[2 * e + 1]), sl2x2, nm2);
-            float2 p;
-            // polynomial pairs: the last EMU of every 8, or (DA_EMU_SPREAD) spread evenly so the
-            // MUFU and FMA-pipe instructions interleave in each warp's stream
-            if (DA_EMU_SPREAD ? ((e * EMU) & 7) < EMU : (e & 7) >= 8 - EMU)
-              p = exp2_poly2(x);
-            else
-              p = make_float2(ex2(x.x), ex2(x.y));
-            acc[e & 3] = fadd2(acc[e & 3], p);
-            pr[e] = pack_bf16x2(p.x, p.y);
-            if ((e & 7) == 7)
-              tmem_st8(tmem + lane_base + kColS + 128u * t + (uint32_t)(kPOff * part) + (e - 7), &pr[e - 7]);
-          }
-        };
-        auto zero_acc = [&]() {
-#pragma unroll
-          for (int a = 0; a < 4; ++a) acc[a] = make_float2(0.f, 0.f);
-        };
-        zero_acc();
-        if (kSpec && i > 0) {
-          uint32_t r0[32], r1[32];
-          tmem_ld32(tS, r0);
-          tmem_ld_wait(r0);
-          tmem_ld32(tS + 32u, r1);  // drains under the first half's exps
-          take(r0, 0);
-          exps(0, 16);
-          float mx = rmax(0, 32);
-          tmem_ld_wait(r1);
-          take(r1, 1);
-          exps(16, 32);
-          mx = fmaxf(mx, rmax(32, 32));
-          mx = exchange(mx);
-          DA_TRACE(3 * t + 1, i, row == 0 && part == 0);
-          if (rescale(fmaxf(m[t], mx * sl2))) {  // rare: redo the tile against the new max
-            zero_acc();
-            exps(0, CW / 2);
-          }
+        for (int o = 1; o < kSplit; ++o) mx = fmaxf(mx, xm[((part + o) % kSplit) * 128]);
+        const float mnew = fmaxf(m[t], mx * sl2);
+        DA_TRACE(3 * t + 1, i, row == 0 && part == 0);
+        if (i == 0) {
+          m[t] = mnew;
         } else {
-          uint32_t sr[CW];
+          // S_t(i) was committed after PV_t(i-1) was issued, so O_t holds sum_{<i} P V.
+          const bool need = mnew > m[t] + 8.0f;
+          if (__any_sync(0xffffffffu, need)) {
+            const float f = need ? ex2(m[t] - mnew) : 1.0f;
 #pragma unroll
-          for (int c = 0; c < CW / 32; ++c) tmem_ld32(tS + 32u * c, *reinterpret_cast<uint32_t(*)[32]>(&sr[32 * c]));
-          tmem_ld_wait();
+            for (int c = 0; c < DP / OC; ++c) {
+              uint32_t r[OC];
+              tmem_ldn<OC>(tO + (uint32_t)(OC * c), r);
+              tmem_ld_wait();
 #pragma unroll
-          for (int c = 0; c < CW / 32; ++c) take(*reinterpret_cast<uint32_t(*)[32]>(&sr[32 * c]), c);
-          const float mx = exchange(rmax(0, CW));
-          const float mnew = fmaxf(m[t], mx * sl2);
-          DA_TRACE(3 * t + 1, i, row == 0 && part == 0);
-          if (i == 0)
-            m[t] = mnew;
+              for (int e = 0; e < OC; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * f);
+              tmem_stn<OC>(tO + (uint32_t)(OC * c), r);
+            }
+            if (need) {
+              l[t] *= f;
+              m[t] = mnew;
+            }
+          }
+        }
+        // p = 2^(s*scale*log2e - m): FFMA2 for the affine part, EMU/8 of the pairs on the FMA
+        // pipe, the rest on MUFU; 4 independent FADD2 partial sums.
+        const float2 sl2x2 = make_float2(sl2, sl2), nm2 = make_float2(-m[t], -m[t]);
+        float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                         make_float2(0.f, 0.f)};
+        uint32_t pr[CW / 2];
+#pragma unroll
+        for (int e = 0; e < CW / 2; ++e) {
+          const float2 x = fma2(make_float2(sv[2 * e], sv[2 * e + 1]), sl2x2, nm2);
+          float2 p;
+          // polynomial pairs: the last EMU of every 8, or (DA_EMU_SPREAD) spread evenly so the
+          // MUFU and FMA-pipe instructions interleave in each warp's stream
+          if (DA_EMU_SPREAD ? ((e * EMU) & 7) < EMU : (e & 7) >= 8 - EMU)
+            p = exp2_poly2(x);
           else
-            rescale(mnew);
-          exps(0, CW / 2);
+            p = make_float2(ex2(x.x), ex2(x.y));
+          acc[e & 3] = fadd2(acc[e & 3], p);
+          pr[e] = pack_bf16x2(p.x, p.y);
+          // P of keys [CW*part, CW*part + CW) -> columns [CW/2*part, CW/2*part + CW/2) of S_t,
+          // stored in 8-column chunks as they complete so the TMEM writes drain under the
+          // remaining exps
+          if ((e & 7) == 7)
+            tmem_st8(tmem + lane_base + kColS + 128u * t + (uint32_t)(CW / 2 * part) + (e - 7), &pr[e - 7]);
         }
         DA_TRACE(16 + t, i, row == 0 && part == 0);
         const float2 a = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
