@@ -58,7 +58,7 @@ def flops(cfg, B, G):
     """Executed MMA FLOP of one forward (DistrAttention: 2*DR + 2*d per (query, key) pair) and
     full-d-equivalent FLOP (4*N*N*d per head) — SURVEY §8(d)."""
     pairs = B * cfg.H * cfg.N * cfg.N * (0.5 if cfg.causal else 1.0)
-    DR = (128 // cfg.block_l) * cfg.d // G
+    DR = max(1, 128 // cfg.block_l) * cfg.d // G
     return pairs * (2 * DR + 2 * cfg.d), pairs * 4 * cfg.d
 
 

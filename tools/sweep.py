@@ -62,7 +62,7 @@ for name, c in cases:
     d_ms, d_attn = timed(lambda e: run(e))
     x_ms, x_attn = timed(lambda e: run(e, True))
     pairs = c.B * c.H * c.N * c.N * (0.5 if c.causal else 1.0)
-    DR = (128 // c.block_l) * c.d // c.group_size
+    DR = max(1, 128 // c.block_l) * c.d // c.group_size
     rec = {"case": name, "B": c.B, "H": c.H, "H_kv": c.H_kv, "N": c.N, "d": c.d, "block_l": c.block_l,
            "G": c.group_size, "causal": c.causal, "dtype": c.dtype,
            "distr_ms": d_ms, "distr_attn_kernel_ms": d_attn, "exact_ms": x_ms, "exact_attn_kernel_ms": x_attn,
