@@ -284,33 +284,29 @@ DA_DEV void qhat_prologue(const AttnArgs& args, uint64_t* bars, const uint8_t* s
   PT(3)
   // Q̂[r][j] = Q[r][perm[j G]] (sampling); block_l = 64 stacks the two hash blocks of a tile
   // block-diagonally (columns [hb*d/G*, (hb+1)*d/G*) of rows of hash block hb, zeros elsewhere).
-  constexpr int CPR = C::DR / 8;
-  constexpr int NCOMBO = 2 * CPR;          // (tile, chunk) pairs
-  constexpr int TPC = NW / NCOMBO;         // threads per pair (rows strided by TPC)
-  const int combo = ht % NCOMBO, rstart = ht / NCOMBO;
-  const int t = combo / CPR, ch = combo % CPR;
-  if (t < ntile && rstart < TPC) {
-    // the 8 source columns of this 16-byte chunk (or -1 = zero) for each row-parity class
-    int src[2][8];
+  // Thread ht owns output column pair p = ht % CP (CP divides NW, so p is fixed for the thread)
+  // and every (NW/CP)-th row: the 32 lanes of a warp gather from one or a few rows of the staged Q
+  // (few bank conflicts) and store 4 bytes each into the swizzled K-major A operand.
+  constexpr int CP = C::DR / 2;
+  static_assert(NW % CP == 0, "column pairs per worker");
+  const int p = ht % CP, j0 = 2 * p;
+  const uint32_t dcol = (uint32_t)((j0 / C::A_BOX_COLS) * C::A_BOX_BYTES + (j0 % C::A_BOX_COLS) * 2);
+  for (int t = 0; t < ntile; ++t) {
 #pragma unroll
-    for (int hbr = 0; hbr < 2; ++hbr)
+    for (int hbr = 0; hbr < (HB == 2 ? 2 : 1); ++hbr) {
+      int src[2];  // source columns of the pair (-1: zero, the off-diagonal block of l = 64)
 #pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const int j = ch * 8 + e, hbj = j / DG, jj = j % DG;
-        src[hbr][e] = (HB == 2 && hbj != hbr) || (HB != 2 && hbr == 1) ? -1 : perm_s[(t * C::HBE + hbj) * D + jj * G];
+      for (int e = 0; e < 2; ++e) {
+        const int j = j0 + e, hbj = j / DG, jj = j % DG;
+        src[e] = (HB == 2 && hbj != hbr) ? -1 : perm_s[(t * C::HBE + hbj) * D + jj * G];
       }
-    const int j0 = ch * 8;
-    const uint32_t dcol = (uint32_t)((j0 / C::A_BOX_COLS) * C::A_BOX_BYTES + (j0 % C::A_BOX_COLS) * 2);
-    for (int r = rstart; r < BM; r += TPC) {
-      const int hbr = HB == 2 ? r / 64 : 0;
-      uint32_t v[8];
-#pragma unroll
-      for (int e = 0; e < 8; ++e) {
-        const int c = src[hbr][e];
-        v[e] = c < 0 ? 0u : *reinterpret_cast<const uint16_t*>(sQ + q_off(t, r, c));
+      const int rlo = HB == 2 ? 64 * hbr : 0, rhi = HB == 2 ? rlo + 64 : BM;
+#pragma unroll 4
+      for (int r = rlo + ht / CP; r < rhi; r += NW / CP) {
+        const uint32_t v0 = src[0] < 0 ? 0u : *reinterpret_cast<const uint16_t*>(sQ + q_off(t, r, src[0]));
+        const uint32_t v1 = src[1] < 0 ? 0u : *reinterpret_cast<const uint16_t*>(sQ + q_off(t, r, src[1]));
+        *reinterpret_cast<uint32_t*>(sA + t * C::A_BYTES + swz(dcol + r * C::A_SW, C::A_SWB)) = v0 | (v1 << 16);
       }
-      *reinterpret_cast<uint4*>(sA + t * C::A_BYTES + swz(dcol + r * C::A_SW, C::A_SWB)) =
-          make_uint4(v[0] | (v[1] << 16), v[2] | (v[3] << 16), v[4] | (v[5] << 16), v[6] | (v[7] << 16));
     }
   }
   fence_proxy_async_smem();
