@@ -194,10 +194,10 @@ DA_DEV void qhat_prologue(const AttnArgs& args, uint64_t* bars, const uint8_t* s
   if (hash) {
     // Projection: unit = (tile, hash block, column pair, group of KG of the 16 projection rows):
     // per row one 4-byte load of the two columns, KG/4 16-byte (broadcast) projection loads, KG
-    // FFMA2. KG = 8 for the per-tile blocks; the 256-row SHARED block has half / a quarter as many
-    // blocks, so it splits the projection rows finer (KG = 4 at d = 128, 2 below) to keep the
-    // chains of all worker threads busy. The groups' KG-bit patterns are OR-ed through smem.
-    constexpr int KG = !C::SHARED ? 8 : (D == 128 ? 4 : 2);
+    // FFMA2. KG = 8 for the per-tile blocks; the 256-row SHARED block has half as many blocks and
+    // takes KG = d/16 (measured hash phase, C3 d=64: KG 2/4/8 = 9.9k/7.8k/10.7k clk; C4 d=128:
+    // KG 4/8 = 12.7k/10.8k clk). The groups' KG-bit patterns are OR-ed through shared memory.
+    constexpr int KG = !C::SHARED ? 8 : D / 16;
     constexpr int NKG = 16 / KG;
     const int nunits = (C::SHARED ? 1 : ntile * HB) * (D / 2) * NKG;  // (hash block, column pair, group)
     uint8_t* parts = reinterpret_cast<uint8_t*>(key_s + 2 * C::HBE * D);  // [block, column][NKG]
