@@ -83,9 +83,15 @@ int distr_attn_init_params(da_params* p, int B, int H, int N, int d, int block_l
 int distr_attn_fwd(const void* q, const void* k, const void* v, void* out, int B, int H, int N,
                    int d, int block_l, int group_size, unsigned long long seed);
 
-/* DistrAttention forward, all options. Launches the LSH/prep kernel (hash -> Gray rank -> stable
- * sort -> sampled Q̂, K^T layout pass) and the fused tcgen05 attention kernel (fusion of K
- * columns per Q block, reduced-d QK^T, online softmax, full-d PV) on `cuda_stream`. */
+/* DistrAttention forward, all options. Launches, on `cuda_stream`:
+ *   bf16 inputs (2 launches): (1) prep_kernel = the K^T layout pass only ([B*H_kv][d][N_pad]
+ *     bf16 in the workspace); (2) the fused tcgen05 attention kernel, whose CTAs each hash their
+ *     own Q blocks in shared memory (projection fp32 fma chain -> sign bits -> inverse Gray ->
+ *     stable rank -> perm -> sampled Q̂; exports bucket_ids / perm when set) and then run the
+ *     per-tile fusion of K columns, the reduced-d QK^T, the online softmax and the full-d PV.
+ *   fp32 inputs (4 launches): a bf16 conversion of V; prep_kernel hashing the fp32 Q blocks
+ *     (-> perm workspace + exports) and the K^T pass; a bf16 conversion of Q; the attention
+ *     kernel reading the perm instead of hashing. */
 int distr_attn_fwd_ex(const void* q, const void* k, const void* v, void* out, const da_params* p,
                       void* cuda_stream);
 
@@ -118,10 +124,13 @@ int distr_attn_global_fwd_ex(const void* q, const void* k, const void* v, void* 
  * LSE (da_params.lse of the forward call, [B, H, N] fp32), and dout = dL/dout; outputs dq
  * [B,H,N,d], dk, dv [B,H_kv,N,d] (bf16, overwritten). Same params as the forward (block_l,
  * group_size, seed select the grouping; causal, scale; group_size = 1 gives exact attention
- * gradients). bf16 only. First version: the attention GEMMs run on cuBLAS over chunks of query
- * rows (library-managed workspace, ~2^27 fp32 score entries + fp32 dK/dV accumulators); the
- * grouping, Q̃ expansion, softmax/dscore and the dQ fold are this library's kernels. The call
- * synchronises the stream before returning. */
+ * gradients). bf16 only. d in {64, 128}: six launches of this library's kernels — the prep
+ * hash (perm per Q block), Q̃ (every column replaced by its group representative) + D =
+ * rowsum(dO*O), the LSE padded with +inf, the fused tcgen05 dK/dV kernel, the fused tcgen05 dQ̃
+ * kernel, and the fold of dQ̃ onto the representative columns; stream-ordered, no host sync.
+ * d = 32 (or env DA_BWD_CUBLAS=1): the first version, with the attention GEMMs on cuBLAS over
+ * chunks of query rows; that path synchronises the stream before returning. Both use a
+ * library-managed per-device workspace (grown on first use with a device synchronisation). */
 int distr_attn_bwd_ex(const void* q, const void* k, const void* v, const void* out, const void* dout,
                       const float* lse, void* dq, void* dk, void* dv, const da_params* p, void* cuda_stream);
 

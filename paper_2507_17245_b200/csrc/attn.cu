@@ -2,20 +2,27 @@
 //
 // One CTA = TWO 128-row Q tiles of one (b, h) (the outer loop of Fig. 3, two
 // iterations per CTA); the inner loop walks 128-key tiles that both Q tiles share in smem.
-// Warp roles (384 threads):
-//   warp 0      TMA producer: Q (exact) or Q̂ (distr) of both tiles once, then K (exact) or K^T
-//               (distr) tiles through an NS-stage mbarrier ring; warp 2: the V ring.
-//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer, ping-ponging the two tiles:
+// Warp roles (exact: 384 threads; distr: 512):
+//   warp 0      TMA producer of the K ring: K tiles (exact, K-major SW128) or K^T tiles (distr,
+//               128 keys x d rows). The A operand (Q for exact; the natural Q tiles the distr
+//               prologue hashes) is loaded once by thread 0 before the roles start.
+//   warp 1      TMEM allocator (512 columns) + single-thread tcgen05.mma issuer, in the order
+//               PV_0(i-1), S_0(i), PV_1(i-1), S_1(i):
 //                 S_t  = A_t · B_t^T        (M=128, N=128, K = d or DR = HB*d/G*; fp32 in TMEM)
 //                 O_t += P_t · V            (A = P_t bf16 read from TMEM, B = V MN-major, N = d)
-//   warps 2-3   (distr) fusion: K̂_t^T[j][key] = sum_{c in G_j} K^T[c][key] with each tile's own
+//   warp 2      TMA producer of the V ring (SW128); warp 3 idle.
+//   warps 4-11  softmax: all 8 warps work on ONE tile at a time, alternating tiles in the MMA's
+//               order, so tile t's exp phase overlaps the tensor core's work on tile 1-t. Warps
+//               w and w+4 own the same 32 TMEM lanes (query rows) and split the 128 key columns;
+//               row max combined through smem; lazy O rescale (only when the running max grows
+//               by > 2^8); exp2 on MUFU plus an FMA-pipe polynomial for EMU/8 of the pairs; P ->
+//               TMEM (bf16) in 8-column chunks; O / l epilogue.
+//   warps 12-15 (distr) fusion: K̂_t^T[j][key] = sum_{c in G_j} K^T[c][key] with each tile's own
 //               permutation(s) — Eq. 2 with the block-wise grouping of §3.3 (P:306:
 //               "the rows of a K block are grouped depending on which Q block is multiplied by").
-//   warps 4-7   softmax warpgroup of tile 0, warps 8-11 of tile 1 (thread = query row = TMEM
-//               lane): row max, exp2 (MUFU + FMA-pipe polynomial), row sum, P -> TMEM (bf16),
-//               lazy O rescale (only when the running max grows by > 2^8), O / l epilogue.
-// While one warpgroup waits for its next S the other runs its exp phase, so the MUFU, the FMA
-// pipe and the tensor core overlap (the FlashAttention-4 ping-pong, re-derived here).
+//   distr prologue (warps 4-15, qhat_prologue): hash the CTA's Q blocks from the staged natural
+//               Q tiles (fp32 fma chain -> sign bits -> inverse Gray -> stable rank -> perm) and
+//               gather Q̂ into the swizzled A operand, before the roles above start.
 // TMEM (512 columns): O_0 [0, d), O_1 [d, 2d), S_0 [256, 384), S_1 [384, 512); P_t aliases the
 // first 64 columns of S_t.
 #include <cuda_bf16.h>

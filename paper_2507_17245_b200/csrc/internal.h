@@ -18,7 +18,6 @@ struct PrepArgs {
   uint8_t* perm_ws;    // [BH][nqb][d]  (nullable in hash-only mode)
   uint16_t* bucket_out;  // optional export [BH][nqb][d]
   uint8_t* perm_out;     // optional export [BH][nqb][d]
-  uint16_t* qhat;      // [BH][N][DR] bf16 bits (nullable: hash only)
   uint16_t* kt;        // [BHkv][d][N_pad] bf16 bits (nullable)
   int n_hash_ctas;     // BH * nqb (0 = no hashing)
   int n_kt_ctas;       // BHkv * ceil(N/64) (0 = no K^T pass)

@@ -5,9 +5,9 @@
 //                                        fma.rn.f32x2: lane-wise identical to fmaf)
 //   bit_k = y > 0 ; pattern = sum bit_k << k ; bucket = inverse-Gray(pattern)
 //   perm = stable ascending order of (bucket, column) — rank by counting
-//   Q̂[r][j] = Q[r][perm[j*G]] (sampling), written in the tile layout the attention
-//   kernel's TMA reads: [BH][N][DR], DR = HB * d / G, hash block hb of a 128-row tile occupying
-//   columns [hb*d/G, (hb+1)*d/G) and zeros elsewhere (block-diagonal stacking for block_l = 64).
+//   -> perm workspace (fp32 forward, backward) and the optional bucket / perm exports
+//   (distr_attn_hash). The bf16 forward does not launch hash CTAs: its attention CTAs hash their
+//   own Q blocks (attn.cu qhat_prologue, the same arithmetic) and sample Q̂ in shared memory.
 // K^T CTAs, one per (b*H_kv + h, 64-key tile): K [N][d] -> K^T [d][N_pad] (bf16), the layout
 //   in which per-(Q block, K tile) fusion is a sum of whole 16-byte row chunks.
 //
@@ -149,28 +149,6 @@ DA_DEV void hash_cta(const PrepArgs& a, int it, uint8_t* smem) {
   if (threadIdx.x < D) {
     if (a.perm_ws) a.perm_ws[(size_t)it * D + threadIdx.x] = perm_s[threadIdx.x];
     if (a.perm_out) a.perm_out[(size_t)it * D + threadIdx.x] = perm_s[threadIdx.x];
-  }
-  if (!a.qhat) return;
-
-  // Sampling: Q̂ rows of this block, 8 bf16 (16 B) per store; lanes of a warp cover 4 rows.
-  const int dg = D / a.G;
-  const int half = (a.HB == 2) ? (qb & 1) : 0;
-  const int cpr_sh = ilog2(a.DR / 8);  // 16-byte chunks per Q̂ row = DR / 8
-  uint16_t* qh = a.qhat + ((size_t)bh * a.N + r0) * a.DR;
-  for (int i = threadIdx.x; i < (rows << cpr_sh); i += kThreads) {
-    const int r = i >> cpr_sh, ch = i & ((1 << cpr_sh) - 1);
-    uint32_t w[4];
-#pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      uint16_t v2[2];
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int j = ch * 8 + 2 * e + u - half * dg;
-        v2[u] = (j >= 0 && j < dg) ? f2bf(load_f<T>(q_s + r * QP + perm_s[j * a.G])) : (uint16_t)0;
-      }
-      w[e] = (uint32_t)v2[0] | ((uint32_t)v2[1] << 16);
-    }
-    *reinterpret_cast<uint4*>(qh + (size_t)r * a.DR + ch * 8) = make_uint4(w[0], w[1], w[2], w[3]);
   }
 }
 

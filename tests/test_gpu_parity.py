@@ -214,8 +214,8 @@ def test_error_against_exact_is_reported_not_gated():
 
 
 # ------------------------------------------------------------------------------ in-CTA hashing
-# Sequences with more than 8 key tiles hash their Q blocks inside the attention CTA
-# (qhat_prologue); shorter ones in the prep launch. These cases keep the in-CTA path covered.
+# bf16 forwards hash their Q blocks inside the attention CTA (qhat_prologue); these cases check
+# its exports at N=1300 over the kernel envelope (test_gpu_fwd_exports.py covers the configs).
 @pytest.mark.parametrize("d,block_l,G", [(32, 128, 2), (64, 64, 2), (64, 128, 4), (128, 128, 2),
                                          (128, 64, 2), (128, 128, 8), (128, 128, 1), (32, 256, 2),
                                          (64, 256, 4), (128, 256, 2), (128, 256, 4)])

@@ -1,0 +1,9 @@
+#!/bin/bash
+# Baseline pass: GPU tests, smoke, bench, CTA-0 timelines.
+O=gpurun_out/${TAG:-base}; mkdir -p $O
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,driver_version --format=csv > $O/gpu.txt
+timeout -s KILL 1200 python -m pytest tests -m gpu -q -x -p no:cacheprovider > $O/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> $O/pytest_gpu.log
+timeout -s KILL 300 python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1; echo "smoke rc=$?" >> $O/smoke.log
+timeout -s KILL 900 python bench.py > $O/bench.log 2>&1; echo "bench rc=$?" >> $O/bench.log
+timeout -s KILL 60 python tools/trace.py distr > $O/trace_distr.log 2>&1
+timeout -s KILL 60 python tools/trace.py exact > $O/trace_exact.log 2>&1
