@@ -2,11 +2,13 @@
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C5]
 
-A "step" is one pass of the whole hot path (prep/LSH kernel + fused attention kernel) over the
-workload's full batch: B=32, H=32, N=16384, d=128, block_l=128, G*=2 (configs[4]; the largest
-configuration with N=16k, d=128 that fits one B200). For N>1 GPUs (torchrun, one rank per GPU)
-the batch is split by b across ranks (strong scaling, no collective in the data path); the
-step time is the max over ranks of CUDA-event time.
+A "step" is one pass of the whole hot path (K^T prep kernel + fused attention kernel with the
+in-CTA LSH) over the workload's full batch: B=32, H=32, N=16384, d=128, block_l=128, G*=2
+(configs[4]; the largest configuration with N=16k, d=128 that fits one B200). For N>1 GPUs
+(torchrun, one rank per GPU) the (b, h) problems are split across ranks — by batch when B
+divides, else by flattened KV heads (strong scaling, no collective in the data path); the step
+time is the max over ranks of CUDA-event time. After the timed region every rank's sampled
+output blocks are gathered to rank 0 over NCCL and checked against the CPU oracle there.
 
 metric/unit follow BASELINE.json: attention forward time in ms (lower is better); the same line
 reports the own exact-kernel time on the same tiling, the tensor-core roofline of the dominant
@@ -34,6 +36,9 @@ sys.path.insert(0, ROOT)
 
 from synth import CONFIGS, make_qkv  # noqa: E402
 
+SM_COUNT = 148
+TC_FLOP_PER_CLK_SM = 8192  # dense bf16 tcgen05, cta_group::1 (B200_PROFILING.md)
+
 METRIC = "attn fwd ms & tensor-pipe util at N=16k,d=128 vs own exact kernel; max abs err"
 
 
@@ -45,6 +50,32 @@ def load_peaks():
     except Exception:
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
                 "sm_max_mhz": 1965.0}, "fallback"
+
+
+def kernel_src_sha():
+    """sha256 (16 hex) of the attention-kernel sources: a stored ncu figure is only reported for the
+    build it was captured on."""
+    import hashlib
+    h = hashlib.sha256()
+    for f in ("attn.cu", "ptx.cuh", "prep.cu", "internal.h"):
+        with open(os.path.join(ROOT, "paper_2507_17245_b200", "csrc", f), "rb") as fh:
+            h.update(fh.read())
+    return h.hexdigest()[:16]
+
+
+def load_traffic(config):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the attention kernel, from the
+    `ncu --set full` capture committed under profiles/ (tools/ncu_traffic.py writes it) — only if
+    it was captured on these kernel sources; else null."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    try:
+        with open(path) as f:
+            rec = json.load(f)
+    except Exception:
+        return None, None
+    if rec.get("kernel_src_sha") != kernel_src_sha():
+        return None, f"stale ({os.path.relpath(path, ROOT)} is for another build)"
+    return rec.get(f"{config}_attn_bytes_per_launch"), rec.get("source")
 
 
 def dist_env():
@@ -162,6 +193,12 @@ def run_reference(args, cfg):
     print(json.dumps(line), flush=True)
 
 
+def pct(xs):
+    xs = np.asarray(xs, dtype=np.float64)
+    return {"p10": float(np.percentile(xs, 10)), "p50": float(np.percentile(xs, 50)),
+            "p90": float(np.percentile(xs, 90)), "mean": float(xs.mean())}
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -189,17 +226,27 @@ def main():
     if world > 1:
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
-    from paper_2507_17245_b200.shard import batch_shard, max_over_ranks, q_pair_shard, q_rows_of_shard
-    if args.shard == "q":  # every rank holds the whole batch and computes its Q tile pairs
-        b0, B = 0, cfg.B
-        qsh = q_pair_shard(rank, world) if world > 1 else None
-    else:
-        b0, B = batch_shard(cfg.B, rank, world)
-        qsh = None
+    from paper_2507_17245_b200.shard import (batch_shard, head_shard, make_head_shard, max_over_ranks,
+                                             q_pair_shard, q_rows_of_shard)
     G = cfg.group_size
-    q, k, v = make_qkv(cfg, device=dev, B=B, head_offset=b0)
+    qsh = None
+    if args.shard == "q":  # every rank holds the whole batch and computes its Q tile pairs
+        q, k, v = make_qkv(cfg, device=dev)
+        qsh = q_pair_shard(rank, world) if world > 1 else None
+        heads = (0, cfg.B * cfg.H)  # flattened q heads this rank holds
+        B_rank = cfg.B
+    elif cfg.B % world == 0:  # (b, h) sharding by batch
+        b0, B_rank = batch_shard(cfg.B, rank, world)
+        q, k, v = make_qkv(cfg, device=dev, B=B_rank, head_offset=b0)
+        heads = (b0 * cfg.H, (b0 + B_rank) * cfg.H)
+    else:  # (b, h) sharding by flattened KV heads (any B)
+        u0, u1 = head_shard(cfg.B, cfg.H, cfg.H_kv, rank, world)
+        q, k, v = make_head_shard(cfg, u0, u1, device=dev)
+        g = cfg.H // cfg.H_kv
+        heads = (u0 * g, u1 * g)
+        B_rank = (u1 - u0) * g / cfg.H
     out = torch.empty_like(q)
-    ws = torch.empty(da.distr_attn_workspace_size(tuple(q.shape), cfg.H_kv, block_l=cfg.block_l,
+    ws = torch.empty(da.distr_attn_workspace_size(tuple(q.shape), k.shape[1], block_l=cfg.block_l,
                                                   group_size=G), dtype=torch.uint8, device=dev)
     stream = torch.cuda.current_stream()
     L = _native.lib()
@@ -238,46 +285,86 @@ def main():
         total = t0.elapsed_time(t1)
         attn = [e[1].elapsed_time(e[2]) for e in evs]
         prep = [e[0].elapsed_time(e[1]) for e in evs]
+        per_step = [e[0].elapsed_time(e[2]) for e in evs]
         total, a_ms, p_ms = max_over_ranks([total, np.mean(attn), np.mean(prep)], device=dev)
-        return total / args.steps, a_ms, p_ms, launches_per_step, clk.summary()
+        return (total / args.steps, a_ms, p_ms, launches_per_step, clk.summary(),
+                {"step": pct(per_step), "attn_kernel": pct(attn)})
 
-    ms, attn_ms, prep_ms, lps, clocks = timed(False)
-    ex_ms, ex_attn_ms, _, _, _ = timed(True)
+    ms, attn_ms, prep_ms, lps, clocks, dist_ms = timed(False)
+    ex_ms, ex_attn_ms, _, _, ex_clocks, ex_dist = timed(True)
 
     peaks, peak_src = load_peaks()
-    # FLOPs of this rank's share (whole job / world in both sharding modes)
-    exec_f, full_f = flops(cfg, B, G)
-    exec_f_ex = B * cfg.H * cfg.N * cfg.N * 4 * cfg.d * (0.5 if cfg.causal else 1.0)
+    # executed FLOPs of this rank's share
+    exec_f, full_f = flops(cfg, 1, G)
+    n_heads_rank = (heads[1] - heads[0]) / cfg.H  # in units of batch elements
+    exec_f, full_f = exec_f * n_heads_rank, full_f * n_heads_rank
+    exec_f_ex = n_heads_rank * cfg.H * cfg.N * cfg.N * 4 * cfg.d * (0.5 if cfg.causal else 1.0)
     if args.shard == "q":
         exec_f, full_f, exec_f_ex = exec_f / world, full_f / world, exec_f_ex / world
     peak = peaks.get("bf16_tflops_sustained", peaks["bf16_tflops"])
     achieved = exec_f / (attn_ms * 1e-3) / 1e12
-    traffic = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "ncu_traffic.json")) as f:
-            traffic = json.load(f).get(f"{args.config}_attn_bytes_per_launch")
-    except Exception:
-        pass
+    traffic, traffic_src = load_traffic(args.config)
 
-    # ---------------------------------------------------------------- parity on sampled blocks
+    def pipe_frac(flop, kms, clk):  # tensor-pipe share at the SM clock measured during the run
+        mhz = clk.get("sm_mhz")
+        return None if not mhz else flop / (kms * 1e-3) / (TC_FLOP_PER_CLK_SM * SM_COUNT * mhz * 1e6)
+
+    # ------------------------------------------------------- parity + error vs exact on sampled blocks
+    # Every rank computes its shard; rank 0 gathers sampled blocks of ALL ranks' outputs (NCCL,
+    # outside the timed region) and checks them against the CPU oracle (DistrAttention) and the
+    # exact-attention oracle (reported approximation error).
     parity = None
-    if not args.no_parity and rank == 0:
+    if not args.no_parity:
         sys.path.insert(0, os.path.join(ROOT, "tests"))
-        from gpu_util import errors, gather_items, oracle_items, valid_rows_mask
+        from gpu_util import errors, oracle_items, valid_rows_mask
         from synth import sample_items
         step(False)
         torch.cuda.synchronize()
-        scfg = cfg.with_(B=B)
-        items = sample_items(scfg, n_heads=2, per_head=2)
-        if qsh is not None:  # only blocks of rank 0's shard were computed here
-            own = q_rows_of_shard(cfg.N, 0, world, cfg.causal)
-            items = [(bh, qb) for bh, _ in items[:1] for r0, r1 in own[:2]
-                     for qb in (r0 // cfg.block_l,)]
-        want = oracle_items(q, k, v, items, block_l=cfg.block_l, G=G, causal=cfg.causal)
-        got = gather_items(out, items, cfg.block_l)
-        mx, mean = errors(got, want, valid_rows_mask(items, cfg.N, cfg.block_l, cfg.d))
-        parity = {"max_abs": mx, "mean_abs": mean, "items": len(items),
-                  "tol": {"max_abs": 2e-2, "mean_abs": 2e-3}, "vs": "oracle DistrAttention"}
+        nb_local = heads[1] - heads[0]
+        if qsh is not None:  # rows this rank computed: its first pair, one head
+            own = q_rows_of_shard(cfg.N, rank, world, cfg.causal)
+            local = [(0, own[0][0] // cfg.block_l)]
+        else:
+            lc = cfg.with_(B=1, H=nb_local, H_kv=max(1, nb_local // (cfg.H // cfg.H_kv)))
+            local = sample_items(lc, n_heads=2, per_head=2, seed=7 + rank)
+        flat = out.reshape(-1, cfg.N, cfg.d)
+        blk = torch.zeros((len(local), cfg.block_l, cfg.d), dtype=out.dtype, device=dev)
+        for j, (bh, qb) in enumerate(local):
+            r0, r1 = qb * cfg.block_l, min(cfg.N, (qb + 1) * cfg.block_l)
+            blk[j, :r1 - r0] = flat[bh, r0:r1]
+        idx = torch.tensor([[heads[0] + bh, qb] for bh, qb in local], dtype=torch.int64, device=dev)
+        if world > 1:
+            blks = [torch.empty_like(blk) for _ in range(world)]
+            idxs = [torch.empty_like(idx) for _ in range(world)]
+            torch.distributed.all_gather(blks, blk)
+            torch.distributed.all_gather(idxs, idx)
+        else:
+            blks, idxs = [blk], [idx]
+        if rank == 0:
+            items = [tuple(x) for t in idxs for x in t.cpu().tolist()]
+            got = torch.cat(blks).double().cpu().numpy()
+            # oracle inputs: regenerate each sampled head (same seeded device generator as the
+            # rank that computed it; the oracle receives the exact fp32 upcast)
+            want = np.zeros_like(got)
+            want_ex = np.zeros_like(got)
+            g = cfg.H // cfg.H_kv
+            for j, (bh, qb) in enumerate(items):
+                qh, kh, vh = make_head_shard(cfg, bh // g, bh // g + 1, device=dev)
+                it = [(bh % g, qb)]
+                want[j] = oracle_items(qh, kh, vh, it, block_l=cfg.block_l, G=G, causal=cfg.causal)[0]
+                want_ex[j] = oracle_items(qh, kh, vh, it, block_l=cfg.block_l, G=0, causal=cfg.causal)[0]
+            mask = valid_rows_mask(items, cfg.N, cfg.block_l, cfg.d)
+            mx, mean = errors(got, want, mask)
+            ex_mx, ex_mean = errors(got, want_ex, mask)
+            d_or = (want - want_ex)[mask]
+            parity = {"max_abs": mx, "mean_abs": mean, "items": len(items), "ranks_checked": world,
+                      "tol": {"max_abs": 2e-2, "mean_abs": 2e-3}, "vs": "oracle DistrAttention",
+                      "ok": bool(mx <= 2e-2 and mean <= 2e-3),
+                      "vs_exact": {"gpu_max_abs": ex_mx, "gpu_mean_abs": ex_mean,
+                                   "oracle_distr_max_abs": float(np.abs(d_or).max()),
+                                   "oracle_distr_mean_abs": float(np.abs(d_or).mean()),
+                                   "oracle_distr_rel_fro": float(np.linalg.norm(d_or) /
+                                                                 np.linalg.norm(want_ex[mask]))}}
 
     # ---------------------------------------------------------------- e2e through the host ABI
     e2e = None
@@ -285,9 +372,9 @@ def main():
         qh, kh, vh = (t.cpu().pin_memory() for t in (q, k, v))
         oh = torch.empty_like(qh).pin_memory()
         da.distr_attn_fwd_host(qh, kh, vh, oh, block_l=cfg.block_l, group_size=G, q_shard=qsh)  # warm
+        host_launches = da.last_launch_count()
         n_e2e = max(1, min(args.steps, 3))
         barrier()
-        t0 = time.perf_counter()
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
@@ -296,11 +383,14 @@ def main():
         e1.record(stream)
         barrier()
         e_ms = max_over_ranks([e0.elapsed_time(e1) / n_e2e], device=dev)[0]
+        same = bool(torch.equal(oh, out.cpu())) if qsh is None else None
         nbytes = q.numel() * q.element_size()
-        e2e = {"value": e_ms, "unit": "ms", "h2d_bytes_per_step": 3 * nbytes * world,
-               "d2h_bytes_per_step": nbytes * world, "steps": n_e2e,
+        kvbytes = k.numel() * k.element_size()
+        e2e = {"value": e_ms, "unit": "ms", "h2d_bytes_per_step": (nbytes + 2 * kvbytes) * world,
+               "d2h_bytes_per_step": nbytes * world, "steps": n_e2e, "kernel_launches": host_launches,
+               "bit_identical_to_device_path": same,
                "note": "q-sharded: every rank copies the whole batch in and out" if qsh else None,
-               "api": "distr_attn_fwd_host (pinned host buffers)"}
+               "api": "distr_attn_fwd_host (pinned host buffers; chunked H2D / compute / D2H overlap)"}
         del qh, kh, vh, oh
 
     # ---------------------------------------------------------------- CPU oracle baseline
@@ -308,7 +398,7 @@ def main():
     if not args.no_cpu and rank == 0 and world == 1:
         import oracle
         n = max(4, min(2 * oracle.num_threads(), 64))
-        dt, n, cores = oracle_sample_time(cfg.with_(B=B), q, k, v, G, n)
+        dt, n, cores = oracle_sample_time(cfg.with_(B=int(B_rank) or 1), q, k, v, G, n)
         total_items = cfg.B * cfg.H * cfg.nqb
         cpu = {"value": dt / n * total_items * 1e3, "unit": "ms", "cores": cores, "kind": "oracle",
                "sample": f"{n} Q blocks of the workload timed ({dt:.1f} s), extrapolated "
@@ -319,16 +409,22 @@ def main():
             "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": bench_config(cfg, G, B, world, args.shard),
+            "config": bench_config(cfg, G, B_rank, world, args.shard),
             "exact_ms": ex_ms, "speedup_vs_exact": ex_ms / ms,
             "attn_kernel_ms": attn_ms, "prep_kernel_ms": prep_ms, "exact_kernel_ms": ex_attn_ms,
+            "percentiles_ms": {"distr": dist_ms, "exact": ex_dist},
             "tflops_executed": exec_f * world / (ms * 1e-3) / 1e12,
             "tflops_full_d_equiv": full_f * world / (ms * 1e-3) / 1e12,
             "roofline": {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
-                         "frac": achieved / peak, "traffic": traffic,
-                         "kernel": "attn_kernel<128,distr,G=2>",
-                         "peak_source": f"{peak_src} bf16_tflops_sustained"},
+                         "frac": achieved / peak, "traffic": traffic, "traffic_source": traffic_src,
+                         "kernel": f"attn_kernel<{cfg.d},distr,G={G}>",
+                         "peak_source": f"{peak_src} bf16_tflops_sustained",
+                         "tensor_pipe_frac_at_clock": pipe_frac(exec_f, attn_ms, clocks),
+                         "tensor_pipe_frac_at_clock_note":
+                             f"executed FLOP/s / ({TC_FLOP_PER_CLK_SM} FLOP/clk/SM x {SM_COUNT} SMs x "
+                             "the median SM clock sampled during the timed region)"},
             "exact_roofline_frac": exec_f_ex / (ex_attn_ms * 1e-3) / 1e12 / peak,
+            "exact_tensor_pipe_frac_at_clock": pipe_frac(exec_f_ex, ex_attn_ms, ex_clocks),
             "parity": parity, "e2e": e2e, "cpu_baseline": cpu, "clocks": clocks,
             "gpu_launches": lps * args.steps,
         }

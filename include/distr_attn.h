@@ -15,14 +15,19 @@
  *     (DA_BF16: bfloat16, DA_F32: float; fp32 inputs are hashed in fp32 and rounded to bf16
  *     for the tensor-core contractions, output written in fp32).
  *   - The caller owns q, k, v, out, lse and the export buffers; the library owns its projection
- *     cache and (when workspace == NULL) a grow-only device workspace pool per device.
+ *     cache and, when workspace == NULL, stream-ordered scratch: cudaMallocAsync on the call's
+ *     stream before the launches and cudaFreeAsync after them, from the device's default memory
+ *     pool (its release threshold is raised once per device, so steady-state calls neither
+ *     cudaMalloc nor synchronise). The first use of a (seed, block_l) projection allocates and
+ *     uploads it synchronously (cudaMalloc + cudaMemcpy) — do that once before graph capture.
  *   - Calls are stream-ordered and asynchronous (`cuda_stream` is a cudaStream_t, NULL = legacy
  *     default stream); synchronisation is the caller's job. Nothing throws across the ABI.
  *   - Every argument is validated before anything is enqueued. On DA_ERR_INVALID /
  *     DA_ERR_PRECONDITION nothing was enqueued and `out` is untouched. DA_ERR_CUDA means a CUDA
  *     call failed (detail in distr_attn_last_error()); `out` is then unspecified.
- *   - Thread safety: the projection cache and workspace pool are mutex-protected; concurrent
- *     calls that share a library-managed workspace on one device must use one stream.
+ *   - Thread safety: the projection cache is mutex-protected; library scratch is per call and
+ *     stream-ordered, so concurrent calls on different streams / host threads never share it. A
+ *     caller-owned workspace must not be used by two calls that can run concurrently.
  *
  * Supported envelope: d in {32, 64, 128}; block_l in {64, 128, 256}; G* (group_size) in {1, 2, 4, 8}
  * with d % G* == 0 and the reduced width max(1, 128 / block_l) * d / G* in [16, 128]; block_l = 256
@@ -95,10 +100,16 @@ int distr_attn_fwd(const void* q, const void* k, const void* v, void* out, int B
 int distr_attn_fwd_ex(const void* q, const void* k, const void* v, void* out, const da_params* p,
                       void* cuda_stream);
 
-/* Same as distr_attn_fwd_ex, but q/k/v/out (and lse/bucket_ids/perm if set) are HOST pointers:
- * the call copies inputs to a library-owned device staging area, runs the forward and copies the
- * result back, all on `cuda_stream`, and returns after the stream has synchronised. Host buffers
- * should be pinned (cudaHostAlloc / torch pin_memory) for asynchronous copies. */
+/* Same as distr_attn_fwd_ex, but q/k/v/out (and lse/bucket_ids/perm if set) are HOST pointers.
+ * The job is cut into chunks of whole KV heads (b, h_kv) with their query heads; per chunk the
+ * inputs are copied to a library-owned device staging slot on an internal copy stream, the
+ * forward runs on `cuda_stream`, and the results are copied back on a second internal copy
+ * stream, through 3 slots, so the copies of neighbouring chunks overlap the kernels (the
+ * double buffering of P:749). Bit-identical to distr_attn_fwd_ex on the same data. With a
+ * Q-tile-pair shard only the shard's rows of out / lse (and its blocks of the exports) are
+ * written. Returns after all work has completed. Host buffers should be pinned (cudaHostAlloc /
+ * torch pin_memory), otherwise the copies are synchronous. One host call runs at a time per
+ * process (internal mutex). */
 int distr_attn_fwd_host(const void* q, const void* k, const void* v, void* out,
                         const da_params* p, void* cuda_stream);
 
@@ -129,8 +140,8 @@ int distr_attn_global_fwd_ex(const void* q, const void* k, const void* v, void* 
  * rowsum(dO*O), the LSE padded with +inf, the fused tcgen05 dK/dV kernel, the fused tcgen05 dQ̃
  * kernel, and the fold of dQ̃ onto the representative columns; stream-ordered, no host sync.
  * d = 32 (or env DA_BWD_CUBLAS=1): the first version, with the attention GEMMs on cuBLAS over
- * chunks of query rows; that path synchronises the stream before returning. Both use a
- * library-managed per-device workspace (grown on first use with a device synchronisation). */
+ * chunks of query rows; that path synchronises the stream before returning. Workspace: the caller's
+ * (p->workspace, >= distr_attn_bwd_workspace_size(p) bytes) or stream-ordered library scratch. */
 int distr_attn_bwd_ex(const void* q, const void* k, const void* v, const void* out, const void* dout,
                       const float* lse, void* dq, void* dk, void* dv, const da_params* p, void* cuda_stream);
 
@@ -142,9 +153,12 @@ int distr_attn_hash(const void* q, const da_params* p, void* cuda_stream);
  * row-major [k][r]. SplitMix64 counter stream + Box-Muller in double rounded to fp32 (R4). */
 int distr_attn_projection(unsigned long long seed, int block_l, float* host_out);
 
-/* Device workspace bytes needed by distr_attn_fwd_ex / exact_attn_fwd_ex for these params
- * (0 if the params are invalid). */
+/* Device workspace bytes needed by distr_attn_fwd_ex / exact_attn_fwd_ex /
+ * distr_attn_global_fwd_ex for these params (0 if the params are invalid). Host-only. */
 size_t distr_attn_workspace_size(const da_params* p);
+
+/* Device workspace bytes distr_attn_bwd_ex needs for these params (0 if invalid). Host-only. */
+size_t distr_attn_bwd_workspace_size(const da_params* p);
 
 /* Block-size planner: the B200 analogue of "Block size selection" (§3.3.1, Eq. 4-5,
  * Table 2). Host-only (no CUDA call, no GPU needed). For (N, d, block_l, group_size, distr) it

@@ -20,7 +20,7 @@ __all__ = [
     "distr_attn_fwd", "distr_attn_fwd_ex", "exact_attn_fwd_ex", "distr_attn_fwd_host",
     "distr_attn_hash", "distr_attn_projection", "distr_attn_workspace_size", "make_params",
     "DistrAttnError", "last_launch_count", "distr_attn_plan", "distr_attn_global_fwd_ex",
-    "distr_attn_bwd_ex",
+    "distr_attn_bwd_ex", "distr_attn_bwd_workspace_size",
 ]
 
 _DT = {torch.bfloat16: DA_BF16, torch.float32: DA_F32}
@@ -44,6 +44,25 @@ def make_params(q: torch.Tensor, k: torch.Tensor, *, block_l: int, group_size: i
     if q.dtype not in _DT:
         raise ValueError(f"unsupported dtype {q.dtype}")
     B, H, N, d = q.shape
+    nqb = -(-N // block_l) if block_l > 0 else 0
+    if lse is not None and (lse.dtype != torch.float32 or tuple(lse.shape) != (B, H, N)):
+        raise ValueError(f"lse must be fp32 [B, H, N] = {(B, H, N)}")
+    for name, t, dts in (("bucket_ids", bucket_ids, (torch.int16, torch.uint16)),
+                         ("perm", perm, (torch.uint8,))):
+        if t is not None and (t.dtype not in dts or t.numel() != B * H * nqb * d):
+            raise ValueError(f"{name} must be {dts[0]} with B*H*ceil(N/block_l)*d = "
+                             f"{B * H * nqb * d} elements")
+    # every tensor the kernels touch: contiguous, and on the same side as q (device: q's device,
+    # which must be the current one)
+    for t in (q, k, v, out, lse, bucket_ids, perm, workspace):
+        if t is None:
+            continue
+        if not t.is_contiguous():
+            raise ValueError("tensors must be contiguous")
+        if t.is_cuda != q.is_cuda or (q.is_cuda and t.device != q.device):
+            raise ValueError("all tensors must live on q's device (or all on the host)")
+    if q.is_cuda and q.device.index != torch.cuda.current_device():
+        raise ValueError(f"q is on {q.device} but the current device is cuda:{torch.cuda.current_device()}")
     p = DaParams()
     p.B, p.H, p.H_kv, p.N, p.d = B, H, k.shape[1], N, d
     p.block_l, p.group_size, p.seed = block_l, group_size, seed
@@ -92,21 +111,19 @@ def distr_attn_global_fwd_ex(q, k, v, out=None, *, group_size=2, seed=0, causal=
     bucket_ids / perm exports are [B, H, 1, d]. Returns `out`."""
     _check_tensors(q, k, v, out, lse)
     B, H, N, d = q.shape
-    for t in (bucket_ids, perm):
-        if t is not None and (t.numel() < B * H * d or not t.is_contiguous()):
-            raise ValueError("bucket_ids / perm exports must be contiguous [B, H, 1, d]")
     if out is None:
         out = torch.empty_like(q)
-    p = make_params(q, k, block_l=128, group_size=group_size, seed=seed, causal=causal,
+    p = make_params(q, k, block_l=N, group_size=group_size, seed=seed, causal=causal,
                     scale=scale, lse=lse, bucket_ids=bucket_ids, perm=perm, workspace=workspace,
                     v=v, out=out, q_shard=q_shard)
+    p.block_l = 128  # not used by the global variant (its tiles are 128 rows)
     check(_native.lib().distr_attn_global_fwd_ex(_ptr(q), _ptr(k), _ptr(v), _ptr(out), ctypes.byref(p),
                                                  _stream(stream)))
     return out
 
 
 def distr_attn_bwd_ex(q, k, v, out, dout, lse, *, block_l=128, group_size=2, seed=0, causal=False,
-                      scale=0.0, stream=None):
+                      scale=0.0, workspace=None, stream=None):
     """Backward of DistrAttention (grouping held constant, reading R18): returns (dq, dk, dv).
     `out` and `lse` ([B, H, N] fp32, natural log) come from the forward call with the same
     params; group_size=1 gives exact-attention gradients."""
@@ -117,7 +134,7 @@ def distr_attn_bwd_ex(q, k, v, out, dout, lse, *, block_l=128, group_size=2, see
         raise ValueError("dout must match q")
     dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
     p = make_params(q, k, block_l=block_l, group_size=group_size, seed=seed, causal=causal,
-                    scale=scale, v=v, out=out)
+                    scale=scale, v=v, out=out, workspace=workspace)
     check(_native.lib().distr_attn_bwd_ex(_ptr(q), _ptr(k), _ptr(v), _ptr(out), _ptr(dout), _ptr(lse),
                                           _ptr(dq), _ptr(dk), _ptr(dv), ctypes.byref(p),
                                           _stream(stream)))
@@ -189,6 +206,15 @@ def distr_attn_workspace_size(q_shape, kv_heads, *, block_l=128, group_size=2,
     p.B, p.H, p.H_kv, p.N, p.d = B, H, kv_heads, N, d
     p.block_l, p.group_size, p.dtype = block_l, group_size, _DT[dtype]
     return int(_native.lib().distr_attn_workspace_size(ctypes.byref(p)))
+
+
+def distr_attn_bwd_workspace_size(q_shape, kv_heads, *, block_l=128, group_size=2,
+                                  dtype=torch.bfloat16) -> int:
+    B, H, N, d = q_shape
+    p = DaParams()
+    p.B, p.H, p.H_kv, p.N, p.d = B, H, kv_heads, N, d
+    p.block_l, p.group_size, p.dtype = block_l, group_size, _DT[dtype]
+    return int(_native.lib().distr_attn_bwd_workspace_size(ctypes.byref(p)))
 
 
 def distr_attn_plan(N: int, d: int, *, block_l: int = 128, group_size: int = 2, distr: bool = True) -> dict:

@@ -21,7 +21,7 @@ EXPORTED = (
     "exact_attn_fwd_ex", "distr_attn_hash", "distr_attn_projection", "distr_attn_workspace_size",
     "distr_attn_status_string", "distr_attn_last_error", "distr_attn_last_launch_count",
     "distr_attn_set_profile_events", "distr_attn_set_trace", "distr_attn_plan",
-    "distr_attn_global_fwd_ex", "distr_attn_bwd_ex",
+    "distr_attn_global_fwd_ex", "distr_attn_bwd_ex", "distr_attn_bwd_workspace_size",
 )
 
 
@@ -76,6 +76,8 @@ def lib() -> ctypes.CDLL:
             L.distr_attn_projection.argtypes = [ctypes.c_ulonglong, i32, vp]
             L.distr_attn_workspace_size.argtypes = [P]
             L.distr_attn_workspace_size.restype = ctypes.c_size_t
+            L.distr_attn_bwd_workspace_size.argtypes = [P]
+            L.distr_attn_bwd_workspace_size.restype = ctypes.c_size_t
             L.distr_attn_status_string.argtypes = [i32]
             L.distr_attn_status_string.restype = ctypes.c_char_p
             L.distr_attn_last_error.restype = ctypes.c_char_p

@@ -73,23 +73,38 @@ void make_projection(uint64_t seed, int block_l, float* out) {
 }
 
 std::mutex g_mu;
-std::map<std::tuple<int, uint64_t, int>, float*> g_proj;  // (device, seed, block_l) -> device ptr
-struct Pool {
-  void* ptr = nullptr;
-  size_t bytes = 0;
-};
-std::map<int, Pool> g_pool;       // per-device workspace
-std::map<int, Pool> g_host_pool;  // per-device staging for distr_attn_fwd_host
+// (device, seed, block_l) -> device ptr. Block-wise projections (block_l <= 256) are few and kept
+// for the process lifetime; the global variant's [16][N] projections (one per sequence length)
+// are kept in a small LRU: evicting one waits for the device to go idle first (a kernel in
+// flight may still read it).
+std::map<std::tuple<int, uint64_t, int>, float*> g_proj;
+std::vector<std::tuple<int, uint64_t, int>> g_proj_lru;  // global-variant keys, oldest first
+constexpr size_t kGlobalProjKeep = 8;
 
 int get_projection(int dev, uint64_t seed, int block_l, cudaStream_t st, const float** out) {
   std::lock_guard<std::mutex> lk(g_mu);
   auto key = std::make_tuple(dev, seed, block_l);
   auto it = g_proj.find(key);
   if (it != g_proj.end()) {
+    if (block_l > 256) {  // refresh LRU position
+      for (size_t i = 0; i < g_proj_lru.size(); ++i)
+        if (g_proj_lru[i] == key) {
+          g_proj_lru.erase(g_proj_lru.begin() + i);
+          break;
+        }
+      g_proj_lru.push_back(key);
+    }
     *out = it->second;
     return DA_OK;
   }
-  std::vector<float> h(16 * block_l);
+  if (block_l > 256 && g_proj_lru.size() >= kGlobalProjKeep) {
+    const auto old = g_proj_lru.front();
+    DA_CUDA(cudaDeviceSynchronize());
+    DA_CUDA(cudaFree(g_proj[old]));
+    g_proj.erase(old);
+    g_proj_lru.erase(g_proj_lru.begin());
+  }
+  std::vector<float> h(16 * (size_t)block_l);
   make_projection(seed, block_l, h.data());
   float* d = nullptr;
   DA_CUDA(cudaMalloc(&d, h.size() * sizeof(float)));
@@ -97,24 +112,39 @@ int get_projection(int dev, uint64_t seed, int block_l, cudaStream_t st, const f
   DA_CUDA(cudaMemcpy(d, h.data(), h.size() * sizeof(float), cudaMemcpyHostToDevice));
   (void)st;
   g_proj[key] = d;
+  if (block_l > 256) g_proj_lru.push_back(key);
   *out = d;
   return DA_OK;
 }
 
-int get_pool(std::map<int, Pool>& pools, int dev, size_t need, void** out) {
-  std::lock_guard<std::mutex> lk(g_mu);
-  Pool& p = pools[dev];
-  if (p.bytes < need) {
-    if (p.ptr) {
-      DA_CUDA(cudaDeviceSynchronize());
-      DA_CUDA(cudaFree(p.ptr));
-      p.ptr = nullptr;
-      p.bytes = 0;
-    }
-    DA_CUDA(cudaMalloc(&p.ptr, need));
-    p.bytes = need;
+// Library-managed scratch is stream-ordered: cudaMallocAsync on the call's stream before the
+// launches, cudaFreeAsync after them, from the device's default memory pool (release threshold
+// raised once per device so the pool keeps its memory between calls: no cudaMalloc /
+// synchronisation on the steady-state path). Calls on different streams or host threads never
+// share scratch, and a scratch block is reused only after the stream work that used it.
+struct Scratch {
+  void* p = nullptr;
+  cudaStream_t st = nullptr;
+  ~Scratch() {
+    if (p) cudaFreeAsync(p, st);
   }
-  *out = p.ptr;
+};
+int scratch_alloc(Scratch& sc, size_t bytes, int dev, cudaStream_t st) {
+  {
+    static std::vector<int> configured;
+    std::lock_guard<std::mutex> lk(g_mu);
+    bool done = false;
+    for (int d : configured) done |= d == dev;
+    if (!done) {
+      cudaMemPool_t pool;
+      DA_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+      uint64_t thr = ~0ull;
+      DA_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+      configured.push_back(dev);
+    }
+  }
+  DA_CUDA(cudaMallocAsync(&sc.p, bytes, st));
+  sc.st = st;
   return DA_OK;
 }
 
@@ -265,15 +295,15 @@ int forward(const void* q, const void* k, const void* v, void* out, const da_par
   int dev;
   if (int s = current_device(&dev)) return s;
   uint8_t* ws = nullptr;
+  Scratch sc;  // freed (stream-ordered) after the launches below
   if (P.total) {
     if (p->workspace) {
       if (p->workspace_bytes < P.total)
         return fail(DA_ERR_PRECONDITION, "workspace too small (%zu < %zu)", p->workspace_bytes, P.total);
       ws = static_cast<uint8_t*>(p->workspace);
     } else {
-      void* w;
-      if (int s = get_pool(g_pool, dev, P.total, &w)) return s;
-      ws = static_cast<uint8_t*>(w);
+      if (int s = scratch_alloc(sc, P.total, dev, st)) return s;
+      ws = static_cast<uint8_t*>(sc.p);
     }
   }
   const float* proj = nullptr;
@@ -375,7 +405,10 @@ size_t global_ws_bytes(const Plan& P, size_t* off_qhat, size_t* off_khat) {
 
 int forward_global(const void* q, const void* k, const void* v, void* out, const da_params* p, cudaStream_t st) {
   Plan P;
-  if (int s = validate(p, true, &P)) return s;
+  if (!p) return fail(DA_ERR_INVALID, "params is NULL");
+  da_params pg = *p;  // block_l is not used by the global variant: validate its tiling (128 rows)
+  pg.block_l = 128;
+  if (int s = validate(&pg, true, &P)) return s;
   if (!q || !k || !v || !out) return fail(DA_ERR_INVALID, "null tensor pointer");
   if (P.f32) return fail(DA_ERR_PRECONDITION, "global grouping: bf16 inputs only");
   int dev;
@@ -383,14 +416,14 @@ int forward_global(const void* q, const void* k, const void* v, void* out, const
   size_t off_qh, off_kh;
   const size_t need = global_ws_bytes(P, &off_qh, &off_kh);
   uint8_t* ws;
+  Scratch sc;
   if (p->workspace) {
     if (p->workspace_bytes < need)
       return fail(DA_ERR_PRECONDITION, "workspace too small (%zu < %zu)", p->workspace_bytes, need);
     ws = static_cast<uint8_t*>(p->workspace);
   } else {
-    void* w;
-    if (int s = get_pool(g_pool, dev, need, &w)) return s;
-    ws = static_cast<uint8_t*>(w);
+    if (int s = scratch_alloc(sc, need, dev, st)) return s;
+    ws = static_cast<uint8_t*>(sc.p);
   }
   const float* proj = nullptr;  // one projection over all N rows: (seed, N) -> [16][N]
   if (int s = get_projection(dev, p->seed, P.N, st, &proj)) return s;
@@ -434,7 +467,6 @@ int forward_global(const void* q, const void* k, const void* v, void* out, const
   return DA_OK;
 }
 
-std::map<int, Pool> g_bwd_pool;  // per-device backward workspace
 std::map<int, cublasHandle_t> g_cublas;
 
 int get_cublas(int dev, cublasHandle_t* h) {
@@ -449,21 +481,42 @@ int get_cublas(int dev, cublasHandle_t* h) {
   return DA_OK;
 }
 
+// Backward workspace: the caller's (p->workspace, at least distr_attn_bwd_workspace_size bytes) or
+// stream-ordered library scratch.
+constexpr int kSizeOnly = 100;      // internal status: size query answered, nothing launched
+thread_local bool g_bwd_size_only = false;
+thread_local size_t g_bwd_query = 0;
+int bwd_workspace(const da_params* p, size_t need, int* dev, cudaStream_t st, Scratch& sc, uint8_t** ws) {
+  if (g_bwd_size_only) {
+    g_bwd_query = need;
+    return kSizeOnly;
+  }
+  if (int s = current_device(dev)) return s;
+  if (p->workspace) {
+    if (p->workspace_bytes < need)
+      return fail(DA_ERR_PRECONDITION, "backward workspace too small (%zu < %zu)", p->workspace_bytes, need);
+    *ws = static_cast<uint8_t*>(p->workspace);
+    return DA_OK;
+  }
+  if (int s = scratch_alloc(sc, need, *dev, st)) return s;
+  *ws = static_cast<uint8_t*>(sc.p);
+  return DA_OK;
+}
+
 // Fused tcgen05 backward (bwd_fused.cu): hash -> Q̃ + D + padded lse -> dK/dV kernel -> dQ̃ kernel
 // -> fold. d in {64, 128}.
 int backward_fused(const void* q, const void* k, const void* v, const void* o, const void* dout, const float* lse,
                    void* dq, void* dk, void* dv, const da_params* p, const Plan& P, cudaStream_t st) {
-  int dev;
-  if (int s = current_device(&dev)) return s;
+  int dev = 0;
   const size_t BH = (size_t)P.B * P.H, BHkv = (size_t)P.B * P.Hkv, N = P.N, d = P.d;
   const size_t N_pad = (N + 127) / 128 * 128;
   size_t o_ = 0;
   auto take = [&](size_t bytes) { size_t at = o_; o_ = al256(o_ + bytes); return at; };
   const size_t off_perm = take(BH * P.nqb * d), off_qt = take(BH * N * d * 2), off_D = take(BH * N_pad * 4);
   const size_t off_lse = take(BH * N_pad * 4), off_dqt = take(BH * N * d * 4);
-  void* w;
-  if (int s = get_pool(g_bwd_pool, dev, o_, &w)) return s;
-  uint8_t* ws = static_cast<uint8_t*>(w);
+  Scratch sc;
+  uint8_t* ws;
+  if (int s = bwd_workspace(p, o_, &dev, st, sc, &ws)) return s;
   const float* proj = nullptr;
   if (int s = get_projection(dev, p->seed, P.l, st, &proj)) return s;
   da::PrepArgs pa{};
@@ -510,8 +563,7 @@ int backward(const void* q, const void* k, const void* v, const void* o, const v
   if (int s = validate(p, true, &P)) return s;
   if (!q || !k || !v || !o || !dout || !lse || !dq || !dk || !dv) return fail(DA_ERR_INVALID, "null pointer");
   if (P.f32) return fail(DA_ERR_PRECONDITION, "backward: bf16 tensors only");
-  int dev;
-  if (int s = current_device(&dev)) return s;
+  int dev = 0;
   const size_t BH = (size_t)P.B * P.H, BHkv = (size_t)P.B * P.Hkv, N = P.N, d = P.d;
   if (P.d != 32 && !getenv("DA_BWD_CUBLAS")) return backward_fused(q, k, v, o, dout, lse, dq, dk, dv, p, P, st);
   // d = 32: cuBLAS GEMMs over chunks of R query rows x nb heads (fp32 score tiles <= 2^27 entries)
@@ -525,9 +577,9 @@ int backward(const void* q, const void* k, const void* v, const void* o, const v
   const size_t off_S = take(tile * 4), off_dP = take(tile * 4), off_P16 = take(tile * 2), off_dS = take(tile * 2);
   const size_t off_dqt = take((size_t)nb * R * d * 4), off_dk = take(BH * N * d * 4), off_dv = take(BH * N * d * 4);
   const size_t off_ptr = take(n_it * 11 * nb * sizeof(void*));
-  void* w;
-  if (int s = get_pool(g_bwd_pool, dev, o_, &w)) return s;
-  uint8_t* ws = static_cast<uint8_t*>(w);
+  Scratch sc;
+  uint8_t* ws;
+  if (int s = bwd_workspace(p, o_, &dev, st, sc, &ws)) return s;
   const float* proj = nullptr;
   if (int s = get_projection(dev, p->seed, P.l, st, &proj)) return s;
   cublasHandle_t h;
@@ -562,6 +614,141 @@ int backward(const void* q, const void* k, const void* v, const void* o, const v
   // the pageable pointer table must outlive the async upload
   DA_CUDA(cudaStreamSynchronize(st));
   g_last_launches = -1;  // kernels + cuBLAS calls (not counted)
+  return DA_OK;
+}
+
+// ---------------------------------------------------------------------------- host entry point
+// distr_attn_fwd_host: the job is cut into chunks of whole KV units (u = b*H_kv + h_kv with its
+// H/H_kv query heads: contiguous in Q, K, V, O, lse and the exports), and chunk c runs
+//   H2D(q, k, v of c) on s_in  ->  forward(c) on the caller's stream  ->  D2H(out, ... of c) on s_out
+// through kSlots staging slots, so the copies of chunk c+1 / c-1 overlap the kernels of chunk c
+// (the paper's copy/compute double buffering). Each chunk is one forward call over
+// B = 1, H = units * H/H_kv, H_kv = units (flattened heads; bit-identical to the one-call result:
+// every (b, h) problem is independent). One host call at a time (the call is synchronous).
+constexpr int kSlots = 3;
+struct HostPipe {
+  cudaStream_t s_in = nullptr, s_out = nullptr;
+  cudaEvent_t ev_in[kSlots], ev_comp[kSlots], ev_out[kSlots];
+  void* stage = nullptr;
+  size_t bytes = 0;
+};
+std::mutex g_host_mu;
+std::map<int, HostPipe> g_host;
+
+int forward_host(const void* q, const void* k, const void* v, void* out, const da_params* p, cudaStream_t st) {
+  Plan P;
+  if (int s = validate(p, true, &P)) return s;
+  if (!q || !k || !v || !out) return fail(DA_ERR_INVALID, "null tensor pointer");
+  int dev;
+  if (int s = current_device(&dev)) return s;
+  std::lock_guard<std::mutex> lk(g_host_mu);
+  HostPipe& hp = g_host[dev];
+  if (!hp.s_in) {
+    DA_CUDA(cudaStreamCreateWithFlags(&hp.s_in, cudaStreamNonBlocking));
+    DA_CUDA(cudaStreamCreateWithFlags(&hp.s_out, cudaStreamNonBlocking));
+    for (int i = 0; i < kSlots; ++i) {
+      DA_CUDA(cudaEventCreateWithFlags(&hp.ev_in[i], cudaEventDisableTiming));
+      DA_CUDA(cudaEventCreateWithFlags(&hp.ev_comp[i], cudaEventDisableTiming));
+      DA_CUDA(cudaEventCreateWithFlags(&hp.ev_out[i], cudaEventDisableTiming));
+    }
+  }
+  const size_t es = P.f32 ? 4 : 2, g = (size_t)(P.H / P.Hkv), N = P.N, d = P.d;
+  const size_t U = (size_t)P.B * P.Hkv;  // KV units
+  // per-unit bytes of every buffer
+  const size_t uq = g * N * d * es, ukv = N * d * es, ulse = p->lse ? g * N * 4 : 0;
+  const size_t uexp = g * P.nqb * d, ub = p->bucket_ids ? uexp * 2 : 0, up = p->perm ? uexp : 0;
+  // chunking: ~16 chunks for large jobs (copy/compute overlap), at least 8 MB of inputs per chunk
+  const size_t total_in = U * (uq + 2 * ukv);
+  size_t cu = (U + 15) / 16;
+  const size_t min_units = (8u << 20) / (uq + 2 * ukv) + 1;
+  if (cu < min_units) cu = min_units;
+  if (const char* e = getenv("DA_HOST_CHUNK_UNITS")) cu = (size_t)atoll(e) > 0 ? (size_t)atoll(e) : cu;  // tests
+  if (cu > U) cu = U;
+  const size_t nchunks = (U + cu - 1) / cu;
+  const int slots = nchunks < (size_t)kSlots ? (int)nchunks : kSlots;
+  // slot layout: q, k, v, out, lse, buckets, perm of cu units
+  const size_t o_q = 0, o_k = al256(o_q + cu * uq), o_v = al256(o_k + cu * ukv), o_o = al256(o_v + cu * ukv),
+               o_l = al256(o_o + cu * uq), o_b = al256(o_l + cu * ulse), o_p = al256(o_b + cu * ub),
+               slot_bytes = al256(o_p + cu * up);
+  (void)total_in;
+  if (hp.bytes < slot_bytes * slots) {
+    if (hp.stage) {
+      DA_CUDA(cudaDeviceSynchronize());
+      DA_CUDA(cudaFree(hp.stage));
+      hp.stage = nullptr;
+      hp.bytes = 0;
+    }
+    DA_CUDA(cudaMalloc(&hp.stage, slot_bytes * slots));
+    hp.bytes = slot_bytes * slots;
+  }
+  // Q-tile-pair shard: the 256-row pairs this call computes (kernel slot -> pair mapping)
+  std::vector<std::pair<int, int>> rows;  // [r0, r1)
+  const int npairs = (P.nqt + 1) / 2;
+  if (P.pair_stride > 1) {
+    for (int x = 0; x * P.pair_stride < npairs; ++x) {
+      const int slot = x * P.pair_stride + ((x & 1) ? P.pair_stride - 1 - P.pair_off : P.pair_off);
+      if (slot >= npairs) continue;
+      const int pair = P.causal ? npairs - 1 - slot : slot;
+      rows.emplace_back(pair * 256, std::min(P.N, pair * 256 + 256));
+    }
+  }
+  const auto* qh = static_cast<const uint8_t*>(q);
+  const auto* kh = static_cast<const uint8_t*>(k);
+  const auto* vh = static_cast<const uint8_t*>(v);
+  auto* oh = static_cast<uint8_t*>(out);
+  auto* lh = reinterpret_cast<uint8_t*>(p->lse);
+  auto* bh_ = reinterpret_cast<uint8_t*>(p->bucket_ids);
+  auto* ph = reinterpret_cast<uint8_t*>(p->perm);
+  uint8_t* S = static_cast<uint8_t*>(hp.stage);
+  // D2H of [heads][rows_per_head][w] with only the shard's rows (or everything)
+  auto d2h = [&](uint8_t* dst, const uint8_t* src, size_t heads, size_t per_head, size_t row_w, int row_div,
+                 int nrows_total) -> cudaError_t {
+    if (rows.empty() || row_div == 0)
+      return cudaMemcpyAsync(dst, src, heads * per_head, cudaMemcpyDeviceToHost, hp.s_out);
+    for (auto& rr : rows) {
+      const int r0 = rr.first / row_div, r1 = std::min(nrows_total, (rr.second + row_div - 1) / row_div);
+      cudaError_t e = cudaMemcpy2DAsync(dst + r0 * row_w, per_head, src + r0 * row_w, per_head, (r1 - r0) * row_w,
+                                        heads, cudaMemcpyDeviceToHost, hp.s_out);
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  };
+  int launches = 0;
+  for (size_t c = 0; c < nchunks; ++c) {
+    const int sl = (int)(c % slots);
+    const size_t u0 = c * cu, nu = std::min(cu, U - u0);
+    uint8_t* base = S + sl * slot_bytes;
+    if (c >= (size_t)slots) DA_CUDA(cudaStreamWaitEvent(hp.s_in, hp.ev_comp[sl], 0));  // inputs of c - slots consumed
+    DA_CUDA(cudaMemcpyAsync(base + o_q, qh + u0 * uq, nu * uq, cudaMemcpyHostToDevice, hp.s_in));
+    DA_CUDA(cudaMemcpyAsync(base + o_k, kh + u0 * ukv, nu * ukv, cudaMemcpyHostToDevice, hp.s_in));
+    DA_CUDA(cudaMemcpyAsync(base + o_v, vh + u0 * ukv, nu * ukv, cudaMemcpyHostToDevice, hp.s_in));
+    DA_CUDA(cudaEventRecord(hp.ev_in[sl], hp.s_in));
+    DA_CUDA(cudaStreamWaitEvent(st, hp.ev_in[sl], 0));
+    if (c >= (size_t)slots) DA_CUDA(cudaStreamWaitEvent(st, hp.ev_out[sl], 0));  // outputs of c - slots copied out
+    da_params dp = *p;
+    dp.B = 1;
+    dp.H = (int)(nu * g);
+    dp.H_kv = (int)nu;
+    dp.workspace = nullptr;
+    dp.workspace_bytes = 0;
+    dp.lse = p->lse ? reinterpret_cast<float*>(base + o_l) : nullptr;
+    dp.bucket_ids = p->bucket_ids ? reinterpret_cast<unsigned short*>(base + o_b) : nullptr;
+    dp.perm = p->perm ? base + o_p : nullptr;
+    if (int s = forward(base + o_q, base + o_k, base + o_v, base + o_o, &dp, st, true)) return s;
+    launches += g_last_launches;
+    DA_CUDA(cudaEventRecord(hp.ev_comp[sl], st));
+    DA_CUDA(cudaStreamWaitEvent(hp.s_out, hp.ev_comp[sl], 0));
+    const size_t heads = nu * g;
+    DA_CUDA(d2h(oh + u0 * uq, base + o_o, heads, N * d * es, d * es, 1, P.N));
+    if (p->lse) DA_CUDA(d2h(lh + u0 * ulse, base + o_l, heads, N * 4, 4, 1, P.N));
+    if (p->bucket_ids) DA_CUDA(d2h(bh_ + u0 * ub, base + o_b, heads, P.nqb * d * 2, d * 2, P.l, P.nqb));
+    if (p->perm) DA_CUDA(d2h(ph + u0 * up, base + o_p, heads, P.nqb * d, d, P.l, P.nqb));
+    DA_CUDA(cudaEventRecord(hp.ev_out[sl], hp.s_out));
+  }
+  DA_CUDA(cudaStreamSynchronize(hp.s_out));
+  DA_CUDA(cudaStreamSynchronize(st));
+  DA_CUDA(cudaStreamSynchronize(hp.s_in));
+  g_last_launches = launches;
   return DA_OK;
 }
 
@@ -610,36 +797,7 @@ int distr_attn_global_fwd_ex(const void* q, const void* k, const void* v, void* 
 
 int distr_attn_fwd_host(const void* q, const void* k, const void* v, void* out, const da_params* p,
                         void* cuda_stream) {
-  Plan P;
-  if (int s = validate(p, true, &P)) return s;
-  if (!q || !k || !v || !out) return fail(DA_ERR_INVALID, "null tensor pointer");
-  cudaStream_t st = static_cast<cudaStream_t>(cuda_stream);
-  const size_t es = P.f32 ? 4 : 2;
-  const size_t nq = (size_t)P.B * P.H * P.N * P.d * es, nkv = (size_t)P.B * P.Hkv * P.N * P.d * es;
-  const size_t nlse = p->lse ? (size_t)P.B * P.H * P.N * 4 : 0;
-  const size_t nexp = (size_t)P.B * P.H * P.nqb * P.d;
-  const size_t nb = p->bucket_ids ? nexp * 2 : 0, np = p->perm ? nexp : 0;
-  const size_t o_q = 0, o_k = al256(o_q + nq), o_v = al256(o_k + nkv), o_o = al256(o_v + nkv),
-               o_l = al256(o_o + nq), o_b = al256(o_l + nlse), o_p = al256(o_b + nb), tot = al256(o_p + np);
-  int dev;
-  if (int s = current_device(&dev)) return s;
-  void* stage;
-  if (int s = get_pool(g_host_pool, dev, tot, &stage)) return s;
-  uint8_t* S = static_cast<uint8_t*>(stage);
-  DA_CUDA(cudaMemcpyAsync(S + o_q, q, nq, cudaMemcpyHostToDevice, st));
-  DA_CUDA(cudaMemcpyAsync(S + o_k, k, nkv, cudaMemcpyHostToDevice, st));
-  DA_CUDA(cudaMemcpyAsync(S + o_v, v, nkv, cudaMemcpyHostToDevice, st));
-  da_params dp = *p;
-  dp.lse = p->lse ? reinterpret_cast<float*>(S + o_l) : nullptr;
-  dp.bucket_ids = p->bucket_ids ? reinterpret_cast<unsigned short*>(S + o_b) : nullptr;
-  dp.perm = p->perm ? S + o_p : nullptr;
-  if (int s = forward(S + o_q, S + o_k, S + o_v, S + o_o, &dp, st, true)) return s;
-  DA_CUDA(cudaMemcpyAsync(out, S + o_o, nq, cudaMemcpyDeviceToHost, st));
-  if (p->lse) DA_CUDA(cudaMemcpyAsync(p->lse, S + o_l, nlse, cudaMemcpyDeviceToHost, st));
-  if (p->bucket_ids) DA_CUDA(cudaMemcpyAsync(p->bucket_ids, S + o_b, nb, cudaMemcpyDeviceToHost, st));
-  if (p->perm) DA_CUDA(cudaMemcpyAsync(p->perm, S + o_p, np, cudaMemcpyDeviceToHost, st));
-  DA_CUDA(cudaStreamSynchronize(st));
-  return DA_OK;
+  return forward_host(q, k, v, out, p, static_cast<cudaStream_t>(cuda_stream));
 }
 
 int distr_attn_hash(const void* q, const da_params* p, void* cuda_stream) {
@@ -663,6 +821,16 @@ int distr_attn_hash(const void* q, const da_params* p, void* cuda_stream) {
   DA_CUDA(da::launch_prep(a, st));
   g_last_launches = 1;
   return DA_OK;
+}
+
+size_t distr_attn_bwd_workspace_size(const da_params* p) {
+  static char dummy;
+  g_bwd_size_only = true;
+  g_bwd_query = 0;
+  const int s = backward(&dummy, &dummy, &dummy, &dummy, &dummy, reinterpret_cast<const float*>(&dummy), &dummy,
+                         &dummy, &dummy, p, nullptr);
+  g_bwd_size_only = false;
+  return s == kSizeOnly ? g_bwd_query : 0;
 }
 
 int distr_attn_projection(unsigned long long seed, int block_l, float* host_out) {

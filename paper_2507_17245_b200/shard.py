@@ -18,6 +18,38 @@ def batch_shard(B: int, rank: int, world: int) -> tuple[int, int]:
     return rank * per, per
 
 
+def head_shard(B: int, H: int, H_kv: int, rank: int, world: int) -> tuple[int, int]:
+    """[u0, u1) of the flattened KV units u = b*H_kv + h_kv `rank` owns (each unit carries its
+    H/H_kv query heads, flattened q heads [u0*g, u1*g) with g = H/H_kv): contiguous, sizes differ
+    by at most one, any B (no divisibility requirement; SURVEY §8(e) "(batch, head)")."""
+    if world <= 0 or not 0 <= rank < world:
+        raise ValueError(f"bad rank {rank} / world {world}")
+    if H % H_kv:
+        raise ValueError("H must be a multiple of H_kv")
+    U = B * H_kv
+    base, extra = divmod(U, world)
+    u0 = rank * base + min(rank, extra)
+    return u0, u0 + base + (1 if rank < extra else 0)
+
+
+def make_head_shard(cfg, u0: int, u1: int, *, device="cpu", dist: str = "normal"):
+    """Inputs of KV units [u0, u1) as one flattened batch: q [1, (u1-u0)*g, N, d], k/v
+    [1, u1-u0, N, d] — exactly the rows the full single-process tensors hold for those heads
+    (synth.make_qkv draws per batch element, so the covering batch elements are drawn and
+    sliced)."""
+    import torch
+    from synth import make_qkv
+    g = cfg.H // cfg.H_kv
+    b0, b1 = u0 // cfg.H_kv, -(-u1 // cfg.H_kv)
+    q, k, v = make_qkv(cfg, B=b1 - b0, head_offset=b0, device=device, dist=dist)
+    lo = u0 - b0 * cfg.H_kv
+    n = u1 - u0
+    qf = q.reshape(1, -1, cfg.N, cfg.d)[:, lo * g:(lo + n) * g]
+    kf = k.reshape(1, -1, cfg.N, cfg.d)[:, lo:lo + n]
+    vf = v.reshape(1, -1, cfg.N, cfg.d)[:, lo:lo + n]
+    return qf.contiguous(), kf.contiguous(), vf.contiguous()
+
+
 def max_over_ranks(values, device=None):
     """Element-wise max of a list of floats over all ranks (identity without a process group)."""
     import torch

@@ -31,7 +31,7 @@ def header_functions():
 
 def test_exports_every_declared_symbol(L):
     names = header_functions()
-    assert len(names) == 16, names
+    assert len(names) == 17, names
     assert names == set(_native.EXPORTED)
     for n in names:
         assert hasattr(L, n), n
@@ -112,3 +112,34 @@ def test_status_strings(L):
     for s in range(4):
         assert L.distr_attn_status_string(s).decode()
     assert L.distr_attn_status_string(99).decode() == "unknown status"
+
+
+def test_backward_workspace_size_query_is_host_only(L):
+    # fused path (d=128): perm [BH][nqb][d] + Q̃ [BH][N][d] bf16 + D, lse_pad [BH][N_pad128] fp32
+    # + dQ̃ [BH][N][d] fp32
+    p = params(B=2, H=4, N=1000, d=128, block_l=128, G=2)
+    al = lambda x: (x + 255) // 256 * 256
+    BH, N, d, Np = 8, 1000, 128, 1024
+    want = al(BH * 8 * d) + al(BH * N * d * 2) + 2 * al(BH * Np * 4) + al(BH * N * d * 4)
+    assert L.distr_attn_bwd_workspace_size(ctypes.byref(p)) == want
+    assert L.distr_attn_bwd_workspace_size(ctypes.byref(params(d=96))) == 0
+    assert da.distr_attn_bwd_workspace_size((2, 4, 1000, 128), 4) == want
+
+
+def test_binding_rejects_bad_exports_and_lse():
+    import torch
+    q = torch.zeros((1, 2, 100, 64), dtype=torch.bfloat16)
+    with pytest.raises(ValueError, match="lse"):
+        da.make_params(q, q, block_l=64, group_size=2, lse=torch.zeros((1, 2, 99)))
+    with pytest.raises(ValueError, match="lse"):
+        da.make_params(q, q, block_l=64, group_size=2, lse=torch.zeros((1, 2, 100), dtype=torch.float64))
+    with pytest.raises(ValueError, match="bucket_ids"):
+        da.make_params(q, q, block_l=64, group_size=2, bucket_ids=torch.zeros((1, 2, 1, 64), dtype=torch.int16))
+    with pytest.raises(ValueError, match="perm"):
+        da.make_params(q, q, block_l=64, group_size=2, perm=torch.zeros((1, 2, 2, 64), dtype=torch.int16))
+    with pytest.raises(ValueError, match="contiguous"):
+        da.make_params(q, q, block_l=64, group_size=2, lse=torch.zeros((1, 100, 2)).transpose(1, 2))
+    ok = da.make_params(q, q, block_l=64, group_size=2, lse=torch.zeros((1, 2, 100)),
+                        bucket_ids=torch.zeros((1, 2, 2, 64), dtype=torch.int16),
+                        perm=torch.zeros((1, 2, 2, 64), dtype=torch.uint8))
+    assert ok.lse and ok.bucket_ids and ok.perm

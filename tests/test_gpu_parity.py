@@ -253,3 +253,45 @@ def test_block256_fp32_inputs(causal):
     cfg = cfg_small(B=1, H=2, H_kv=1, N=600, d=64, block_l=256, group_size=2, causal=causal, dtype="f32")
     mx, mean, _ = run_and_compare(cfg)
     assert mx <= MAX_ABS and mean <= MEAN_ABS, (mx, mean)
+
+
+@pytest.mark.parametrize("chunk_units", ["1", "3", ""])
+def test_host_entry_point_chunked_pipeline(chunk_units, monkeypatch):
+    # distr_attn_fwd_host cuts the job into chunks of KV heads (H2D / compute / D2H overlap);
+    # whatever the chunking, out, lse and the exports equal the device call bit for bit
+    if chunk_units:
+        monkeypatch.setenv("DA_HOST_CHUNK_UNITS", chunk_units)
+    cfg = cfg_small(B=2, H=4, H_kv=2, N=700, d=128, block_l=128, causal=True)
+    q, k, v = make_qkv(cfg, device=DEV)
+    lse = torch.empty((2, 4, 700), device=DEV)
+    bk = torch.zeros((2, 4, 6, 128), dtype=torch.int16, device=DEV)
+    pm = torch.zeros((2, 4, 6, 128), dtype=torch.uint8, device=DEV)
+    out = da.distr_attn_fwd_ex(q, k, v, block_l=128, group_size=2, seed=5, causal=True, lse=lse,
+                               bucket_ids=bk, perm=pm)
+    torch.cuda.synchronize()
+    qh, kh, vh = (t.cpu().pin_memory() for t in (q, k, v))
+    lh = torch.empty((2, 4, 700)).pin_memory()
+    bh = torch.zeros((2, 4, 6, 128), dtype=torch.int16).pin_memory()
+    ph = torch.zeros((2, 4, 6, 128), dtype=torch.uint8).pin_memory()
+    oh = da.distr_attn_fwd_host(qh, kh, vh, block_l=128, group_size=2, seed=5, causal=True, lse=lh,
+                                bucket_ids=bh, perm=ph)
+    assert torch.equal(oh, out.cpu()) and torch.equal(lh, lse.cpu())
+    assert torch.equal(bh, bk.cpu()) and torch.equal(ph, pm.cpu())
+
+
+def test_host_entry_point_q_shard_writes_only_its_rows(monkeypatch):
+    from paper_2507_17245_b200.shard import q_rows_of_shard
+    monkeypatch.setenv("DA_HOST_CHUNK_UNITS", "2")
+    cfg = cfg_small(B=1, H=4, H_kv=4, N=1100, d=64, block_l=128, causal=True)
+    q, k, v = make_qkv(cfg, device=DEV)
+    full = da.distr_attn_fwd_ex(q, k, v, block_l=128, group_size=2, causal=True)
+    torch.cuda.synchronize()
+    qh, kh, vh = (t.cpu().pin_memory() for t in (q, k, v))
+    oh = torch.full_like(qh, 7.0).pin_memory()
+    da.distr_attn_fwd_host(qh, kh, vh, oh, block_l=128, group_size=2, causal=True, q_shard=(1, 3))
+    rows = q_rows_of_shard(1100, 1, 3, causal=True)
+    mine = torch.zeros(1100, dtype=torch.bool)
+    for r0, r1 in rows:
+        mine[r0:r1] = True
+    assert torch.equal(oh[:, :, mine], full.cpu()[:, :, mine])
+    assert bool((oh[:, :, ~mine] == 7.0).all())

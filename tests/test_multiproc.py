@@ -131,3 +131,60 @@ def test_q_pair_shard_partition_and_causal_balance():
     assert q_pair_shard(3, 8) == (3, 8)
     with pytest.raises(ValueError):
         q_pair_shard(8, 8)
+
+
+# ---------------------------------------------------------------------------------------------
+# flattened (b, h) sharding for any B (no B % world requirement)
+from paper_2507_17245_b200.shard import head_shard, make_head_shard  # noqa: E402
+
+
+def test_head_shard_partition_any_batch():
+    for B, H, Hkv in ((3, 4, 2), (1, 12, 12), (32, 32, 32), (4, 32, 8), (5, 2, 1)):
+        for world in (1, 2, 3, 8):
+            parts = [head_shard(B, H, Hkv, r, world) for r in range(world)]
+            assert parts[0][0] == 0 and parts[-1][1] == B * Hkv
+            assert all(a[1] == b[0] for a, b in zip(parts, parts[1:]))
+            sizes = [u1 - u0 for u0, u1 in parts]
+            assert max(sizes) - min(sizes) <= 1
+
+
+@pytest.mark.parametrize("u0,u1", [(0, 3), (1, 6), (5, 6), (2, 4)])
+def test_make_head_shard_matches_full_tensors(u0, u1):
+    cfg = CONFIGS["C3"].with_(B=3, H=4, H_kv=2, N=33, d=32)
+    q, k, v = make_qkv(cfg)
+    qs, ks, vs = make_head_shard(cfg, u0, u1)
+    g = cfg.H // cfg.H_kv
+    assert torch.equal(qs[0], q.reshape(-1, 33, 32)[u0 * g:u1 * g])
+    assert torch.equal(ks[0], k.reshape(-1, 33, 32)[u0:u1])
+    assert torch.equal(vs[0], v.reshape(-1, 33, 32)[u0:u1])
+
+
+def head_worker(rank, world, port, ret):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import oracle
+    cfg = CONFIGS["C3"].with_(B=3, H=4, H_kv=2, N=70, d=32, block_l=64)  # B=3 over 2 ranks
+    u0, u1 = head_shard(cfg.B, cfg.H, cfg.H_kv, rank, world)
+    q, k, v = make_head_shard(cfg, u0, u1)
+    out = oracle.attn_full(q.float().numpy(), k.float().numpy(), v.float().numpy(),
+                           block_l=cfg.block_l, G=cfg.group_size, causal=True)
+    gathered = [None] * world if rank == 0 else None
+    dist.gather_object((u0, u1, out), gathered, dst=0)
+    if rank == 0:
+        ret["gathered"] = gathered
+    dist.destroy_process_group()
+
+
+def test_world2_flattened_head_shards_match_single_process():
+    world = 2
+    mgr = mp.Manager()
+    ret = mgr.dict()
+    mp.spawn(head_worker, args=(world, free_port(), ret), nprocs=world, join=True)
+    cfg = CONFIGS["C3"].with_(B=3, H=4, H_kv=2, N=70, d=32, block_l=64)
+    q, k, v = make_qkv(cfg)
+    import oracle
+    ref = oracle.attn_full(q.float().numpy(), k.float().numpy(), v.float().numpy(),
+                           block_l=64, G=2, causal=True).reshape(-1, 70, 32)
+    parts = sorted(ret["gathered"], key=lambda x: x[0])
+    full = np.concatenate([o[0] for _, _, o in parts])
+    assert np.array_equal(full, ref)
