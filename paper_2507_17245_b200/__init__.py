@@ -165,7 +165,7 @@ def distr_attn_fwd(q, k, v, out, B, H, N, d, block_l, group_size, seed):
 
 
 def distr_attn_fwd_host(q, k, v, out=None, *, block_l=128, group_size=2, seed=0, causal=False,
-                        scale=0.0, lse=None, stream=None, q_shard=None):
+                        scale=0.0, lse=None, bucket_ids=None, perm=None, stream=None, q_shard=None):
     """Forward over HOST (ideally pinned) tensors: H2D + kernels + D2H inside the C call."""
     for t in (q, k, v):
         if t.is_cuda:
@@ -174,7 +174,8 @@ def distr_attn_fwd_host(q, k, v, out=None, *, block_l=128, group_size=2, seed=0,
     if out is None:
         out = torch.empty_like(q)
     p = make_params(q, k, block_l=block_l, group_size=group_size, seed=seed, causal=causal,
-                    scale=scale, lse=lse, v=v, out=out, q_shard=q_shard)
+                    scale=scale, lse=lse, bucket_ids=bucket_ids, perm=perm, v=v, out=out,
+                    q_shard=q_shard)
     check(_native.lib().distr_attn_fwd_host(_ptr(q), _ptr(k), _ptr(v), _ptr(out), ctypes.byref(p),
                                             _stream(stream)))
     return out

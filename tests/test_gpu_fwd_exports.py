@@ -91,9 +91,10 @@ def test_forward_exports_c4_sweep_points(N, G, block_l):
 
 # ------------------------------------------------------------------------------ stress inputs
 def _cfg(**kw):
-    base = dict(name="s", B=1, H=4, H_kv=4, N=197, d=64, block_l=64, group_size=2, causal=False,
+    base = dict(name="s", B=1, H=4, N=197, d=64, block_l=64, group_size=2, causal=False,
                 dtype="bf16", data_seed=21)
     base.update(kw)
+    base.setdefault("H_kv", base["H"])
     return Config(**base)
 
 
