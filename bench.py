@@ -425,6 +425,8 @@ def main():
                              "the median SM clock sampled during the timed region)"},
             "exact_roofline_frac": exec_f_ex / (ex_attn_ms * 1e-3) / 1e12 / peak,
             "exact_tensor_pipe_frac_at_clock": pipe_frac(exec_f_ex, ex_attn_ms, ex_clocks),
+            "planner": da.distr_attn_choose(cfg.B, cfg.H, cfg.H_kv, cfg.N, cfg.d, causal=cfg.causal,
+                                            max_group_size=G),
             "parity": parity, "e2e": e2e, "cpu_baseline": cpu, "clocks": clocks,
             "gpu_launches": lps * args.steps,
         }

@@ -135,13 +135,12 @@ int distr_attn_global_fwd_ex(const void* q, const void* k, const void* v, void* 
  * LSE (da_params.lse of the forward call, [B, H, N] fp32), and dout = dL/dout; outputs dq
  * [B,H,N,d], dk, dv [B,H_kv,N,d] (bf16, overwritten). Same params as the forward (block_l,
  * group_size, seed select the grouping; causal, scale; group_size = 1 gives exact attention
- * gradients). bf16 only. d in {64, 128}: six launches of this library's kernels — the prep
+ * gradients). bf16 only, d in {32, 64, 128}: six launches of this library's kernels — the prep
  * hash (perm per Q block), Q̃ (every column replaced by its group representative) + D =
  * rowsum(dO*O), the LSE padded with +inf, the fused tcgen05 dK/dV kernel, the fused tcgen05 dQ̃
  * kernel, and the fold of dQ̃ onto the representative columns; stream-ordered, no host sync.
- * d = 32 (or env DA_BWD_CUBLAS=1): the first version, with the attention GEMMs on cuBLAS over
- * chunks of query rows; that path synchronises the stream before returning. Workspace: the caller's
- * (p->workspace, >= distr_attn_bwd_workspace_size(p) bytes) or stream-ordered library scratch. */
+ * Workspace: the caller's (p->workspace, >= distr_attn_bwd_workspace_size(p) bytes) or
+ * stream-ordered library scratch. */
 int distr_attn_bwd_ex(const void* q, const void* k, const void* v, const void* out, const void* dout,
                       const float* lse, void* dq, void* dk, void* dv, const da_params* p, void* cuda_stream);
 
@@ -195,6 +194,26 @@ typedef struct da_plan {
   double hbm_bytes_b200;     /* one head on this kernel: Q + K + V + O (+ K^T write and read, distr) */
 } da_plan;
 int distr_attn_plan(int N, int d, int block_l, int group_size, int distr, da_plan* out);
+
+/* Planner that CHOOSES (the Table 2 step of §3.3.1, decided on B200 by a cost model
+ * calibrated on this build's kernels): for a job (B, H, H_kv, N, d, causal) it
+ * predicts the forward time of the exact kernel and of every DistrAttention setting with
+ * block_l in {64 (d <= 64), 128, 256} and G* in {2, 4, 8} up to max_group_size (the caller's
+ * accuracy bound: G* = 1 is exact attention, error grows with G*, Tables 3-4), and returns the
+ * fastest. Model per CTA (two 128-row Q tiles): prologue clk + key-tile steps x step clk (CTA
+ * timelines, tools/calibrate.sh), CTAs list-scheduled over 148 SMs at clk_mhz (<= 0: 1800), plus
+ * the K^T pass (HBM-bound) and launch overhead. Host-only. Returns DA_OK, DA_ERR_INVALID (NULL
+ * out, non-positive dims, H % H_kv) or DA_ERR_PRECONDITION (d not in {32, 64, 128}). */
+typedef struct da_choice {
+  int distr;                  /* 1: DistrAttention (block_l, group_size below); 0: exact kernel */
+  int block_l;                /* chosen Q-block height (0 when distr = 0) */
+  int group_size;             /* chosen G* (1 when distr = 0) */
+  double predicted_us;        /* predicted forward time of the choice */
+  double predicted_exact_us;  /* predicted forward time of the exact kernel */
+  double predicted_distr_us;  /* fastest DistrAttention setting's predicted time */
+} da_choice;
+int distr_attn_choose(int B, int H, int H_kv, int N, int d, int causal, int max_group_size, double clk_mhz,
+                      da_choice* out);
 
 /* Static description of a status code. */
 const char* distr_attn_status_string(int status);

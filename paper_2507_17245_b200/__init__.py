@@ -20,7 +20,7 @@ __all__ = [
     "distr_attn_fwd", "distr_attn_fwd_ex", "exact_attn_fwd_ex", "distr_attn_fwd_host",
     "distr_attn_hash", "distr_attn_projection", "distr_attn_workspace_size", "make_params",
     "DistrAttnError", "last_launch_count", "distr_attn_plan", "distr_attn_global_fwd_ex",
-    "distr_attn_bwd_ex", "distr_attn_bwd_workspace_size",
+    "distr_attn_bwd_ex", "distr_attn_bwd_workspace_size", "distr_attn_choose",
 ]
 
 _DT = {torch.bfloat16: DA_BF16, torch.float32: DA_F32}
@@ -224,6 +224,16 @@ def distr_attn_plan(N: int, d: int, *, block_l: int = 128, group_size: int = 2, 
     out = _native.DaPlan()
     check(_native.lib().distr_attn_plan(N, d, block_l, group_size, int(distr), ctypes.byref(out)))
     return {name: getattr(out, name) for name, _ in _native.DaPlan._fields_}
+
+
+def distr_attn_choose(B: int, H: int, H_kv: int, N: int, d: int, *, causal: bool = False,
+                      max_group_size: int = 4, clk_mhz: float = 0.0) -> dict:
+    """Planner choice (include/distr_attn.h distr_attn_choose): exact kernel or DistrAttention
+    with (block_l, G* <= max_group_size), by predicted forward time on one B200. Host-only."""
+    out = _native.DaChoice()
+    check(_native.lib().distr_attn_choose(B, H, H_kv, N, d, int(bool(causal)), max_group_size,
+                                          float(clk_mhz), ctypes.byref(out)))
+    return {name: getattr(out, name) for name, _ in _native.DaChoice._fields_}
 
 
 def default_scale(d: int) -> float:

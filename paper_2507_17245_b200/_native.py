@@ -22,6 +22,7 @@ EXPORTED = (
     "distr_attn_status_string", "distr_attn_last_error", "distr_attn_last_launch_count",
     "distr_attn_set_profile_events", "distr_attn_set_trace", "distr_attn_plan",
     "distr_attn_global_fwd_ex", "distr_attn_bwd_ex", "distr_attn_bwd_workspace_size",
+    "distr_attn_choose",
 )
 
 
@@ -43,6 +44,12 @@ class DaPlan(ctypes.Structure):
         "smem_bytes", "tmem_cols", "m_max_tmem", "ctas")] + [(n, ctypes.c_double) for n in (
         "mma_clk_per_tile", "exp_clk_per_tile", "fusion_smem_bytes_per_tile", "hbm_bytes_paper",
         "hbm_bytes_b200")]
+
+
+class DaChoice(ctypes.Structure):
+    _fields_ = [("distr", ctypes.c_int), ("block_l", ctypes.c_int), ("group_size", ctypes.c_int),
+                ("predicted_us", ctypes.c_double), ("predicted_exact_us", ctypes.c_double),
+                ("predicted_distr_us", ctypes.c_double)]
 
 
 class DistrAttnError(RuntimeError):
@@ -86,6 +93,8 @@ def lib() -> ctypes.CDLL:
             L.distr_attn_set_trace.argtypes = [vp]
             L.distr_attn_bwd_ex.argtypes = [vp] * 9 + [P, vp]
             L.distr_attn_plan.argtypes = [i32, i32, i32, i32, i32, ctypes.POINTER(DaPlan)]
+            L.distr_attn_choose.argtypes = [i32, i32, i32, i32, i32, i32, i32, ctypes.c_double,
+                                            ctypes.POINTER(DaChoice)]
             _lib = L
     return _lib
 

@@ -62,7 +62,7 @@ def build(force: bool = False, jobs: int = 4, verbose: bool = False) -> str:
                 sys.stderr.write(log)
     if force or _stale(LIB, objs):
         tmp = LIB + ".tmp"
-        cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs, "-lcublas"]
+        cmd = [NVCC, *ARCH, "-shared", "-o", tmp, *objs]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stderr}")

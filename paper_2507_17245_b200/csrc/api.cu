@@ -3,6 +3,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdlib>
 #include <cstdarg>
@@ -17,7 +18,6 @@
 #include "../../include/distr_attn.h"
 #include "../../include/distr_attn_profile.h"
 #include "internal.h"
-#include <cublas_v2.h>
 
 namespace {
 
@@ -383,6 +383,13 @@ int forward(const void* q, const void* k, const void* v, void* out, const da_par
   aa.lse = p->lse;
   aa.trace = g_trace;
   g_trace = nullptr;
+  // bf16 distr: the attention kernel overlaps the K^T pass (its prologue reads only Q); not when
+  // profile events sit between the two launches (bench.py's kernel split) or DA_PDL=0
+  static const bool pdl_env = [] {
+    const char* e = getenv("DA_PDL");
+    return !(e && e[0] == '0');
+  }();
+  aa.pdl = distr && !P.f32 && pdl_env && !g_ev[1];
   da::AttnLaunch L{P.d, P.G, distr ? P.KHB : 1, distr ? 1 : 0, (int)BH, &tmA, &tmK, &tmV, default_emu(P, distr)};
   record_ev(1, st);
   DA_CUDA(da::launch_attn(L, aa, st));
@@ -467,20 +474,6 @@ int forward_global(const void* q, const void* k, const void* v, void* out, const
   return DA_OK;
 }
 
-std::map<int, cublasHandle_t> g_cublas;
-
-int get_cublas(int dev, cublasHandle_t* h) {
-  std::lock_guard<std::mutex> lk(g_mu);
-  auto it = g_cublas.find(dev);
-  if (it == g_cublas.end()) {
-    cublasHandle_t hh;
-    if (cublasCreate(&hh) != CUBLAS_STATUS_SUCCESS) return fail(DA_ERR_CUDA, "cublasCreate failed");
-    it = g_cublas.emplace(dev, hh).first;
-  }
-  *h = it->second;
-  return DA_OK;
-}
-
 // Backward workspace: the caller's (p->workspace, at least distr_attn_bwd_workspace_size bytes) or
 // stream-ordered library scratch.
 constexpr int kSizeOnly = 100;      // internal status: size query answered, nothing launched
@@ -504,7 +497,7 @@ int bwd_workspace(const da_params* p, size_t need, int* dev, cudaStream_t st, Sc
 }
 
 // Fused tcgen05 backward (bwd_fused.cu): hash -> Q̃ + D + padded lse -> dK/dV kernel -> dQ̃ kernel
-// -> fold. d in {64, 128}.
+// -> fold. d in {32, 64, 128}.
 int backward_fused(const void* q, const void* k, const void* v, const void* o, const void* dout, const float* lse,
                    void* dq, void* dk, void* dv, const da_params* p, const Plan& P, cudaStream_t st) {
   int dev = 0;
@@ -536,10 +529,11 @@ int backward_fused(const void* q, const void* k, const void* v, const void* o, c
   float* lse_pad = reinterpret_cast<float*>(ws + off_lse);
   DA_CUDA(da::launch_bwd_prologue(a, lse, lse_pad, (int)N_pad, st));
   CUtensorMap tmQt, tmdO, tmK, tmV;
-  if (int s = make_map(&tmQt, a.qt, d, N, BH, 64, 128, 128)) return s;
-  if (int s = make_map(&tmdO, dout, d, N, BH, 64, 128, 128)) return s;
-  if (int s = make_map(&tmK, k, d, N, BHkv, 64, 128, 128)) return s;
-  if (int s = make_map(&tmV, v, d, N, BHkv, 64, 128, 128)) return s;
+  const uint32_t rb = d >= 64 ? 64 : (uint32_t)d;  // natural-row boxes: 64 columns (32 for d = 32)
+  if (int s = make_map(&tmQt, a.qt, d, N, BH, rb, 128, (int)rb * 2)) return s;
+  if (int s = make_map(&tmdO, dout, d, N, BH, rb, 128, (int)rb * 2)) return s;
+  if (int s = make_map(&tmK, k, d, N, BHkv, rb, 128, (int)rb * 2)) return s;
+  if (int s = make_map(&tmV, v, d, N, BHkv, rb, 128, (int)rb * 2)) return s;
   da::BwdFusedArgs f{};
   f.tmQt = &tmQt; f.tmdO = &tmdO; f.tmK = &tmK; f.tmV = &tmV;
   f.lse_pad = lse_pad; f.D_pad = a.D;
@@ -563,58 +557,7 @@ int backward(const void* q, const void* k, const void* v, const void* o, const v
   if (int s = validate(p, true, &P)) return s;
   if (!q || !k || !v || !o || !dout || !lse || !dq || !dk || !dv) return fail(DA_ERR_INVALID, "null pointer");
   if (P.f32) return fail(DA_ERR_PRECONDITION, "backward: bf16 tensors only");
-  int dev = 0;
-  const size_t BH = (size_t)P.B * P.H, BHkv = (size_t)P.B * P.Hkv, N = P.N, d = P.d;
-  if (P.d != 32 && !getenv("DA_BWD_CUBLAS")) return backward_fused(q, k, v, o, dout, lse, dq, dk, dv, p, P, st);
-  // d = 32: cuBLAS GEMMs over chunks of R query rows x nb heads (fp32 score tiles <= 2^27 entries)
-  const int R = (int)std::min<size_t>(N, 1024);
-  const int nb = (int)std::max<size_t>(1, std::min<size_t>(BH, ((size_t)1 << 27) / ((size_t)R * N)));
-  const size_t n_it = ((BH + nb - 1) / nb) * ((N + R - 1) / R);
-  size_t o_ = 0;
-  auto take = [&](size_t bytes) { size_t at = o_; o_ = al256(o_ + bytes); return at; };
-  const size_t off_perm = take(BH * P.nqb * d), off_qt = take(BH * N * d * 2), off_D = take(BH * N * 4);
-  const size_t tile = (size_t)nb * R * N;
-  const size_t off_S = take(tile * 4), off_dP = take(tile * 4), off_P16 = take(tile * 2), off_dS = take(tile * 2);
-  const size_t off_dqt = take((size_t)nb * R * d * 4), off_dk = take(BH * N * d * 4), off_dv = take(BH * N * d * 4);
-  const size_t off_ptr = take(n_it * 11 * nb * sizeof(void*));
-  Scratch sc;
-  uint8_t* ws;
-  if (int s = bwd_workspace(p, o_, &dev, st, sc, &ws)) return s;
-  const float* proj = nullptr;
-  if (int s = get_projection(dev, p->seed, P.l, st, &proj)) return s;
-  cublasHandle_t h;
-  if (int s = get_cublas(dev, &h)) return s;
-  // the grouping of every Q block (held constant, R18): the same hash as the forward
-  da::PrepArgs pa{};
-  pa.q = q; pa.k = k; pa.in_f32 = 0;
-  pa.BH = (int)BH; pa.BHkv = (int)BHkv; pa.N = P.N; pa.d = P.d; pa.block_l = P.l; pa.G = P.G; pa.HB = P.HB;
-  pa.DR = P.DR; pa.nqb = P.nqb; pa.N_pad = P.N_pad; pa.proj = proj;
-  pa.perm_ws = ws + off_perm;
-  pa.n_hash_ctas = (int)(BH * P.nqb);
-  DA_CUDA(da::launch_prep(pa, st));
-  da::BwdArgs a{};
-  a.q = static_cast<const uint16_t*>(q); a.k = static_cast<const uint16_t*>(k);
-  a.v = static_cast<const uint16_t*>(v); a.o = static_cast<const uint16_t*>(o);
-  a.dout = static_cast<const uint16_t*>(dout); a.lse = lse; a.perm = ws + off_perm;
-  a.dq = static_cast<uint16_t*>(dq); a.dk = static_cast<uint16_t*>(dk); a.dv = static_cast<uint16_t*>(dv);
-  a.BH = (int)BH; a.BHkv = (int)BHkv; a.H = P.H; a.Hkv = P.Hkv; a.N = P.N; a.d = P.d; a.G = P.G;
-  a.nqb = P.nqb; a.block_l = P.l; a.causal = P.causal; a.scale = P.scale;
-  a.R = R; a.nb = nb;
-  a.qt = reinterpret_cast<uint16_t*>(ws + off_qt); a.D = reinterpret_cast<float*>(ws + off_D); a.Dstride = P.N;
-  a.S = reinterpret_cast<float*>(ws + off_S); a.dP = reinterpret_cast<float*>(ws + off_dP);
-  a.P16 = reinterpret_cast<uint16_t*>(ws + off_P16); a.dS16 = reinterpret_cast<uint16_t*>(ws + off_dS);
-  a.dqt = reinterpret_cast<float*>(ws + off_dqt);
-  a.dk_acc = reinterpret_cast<float*>(ws + off_dk); a.dv_acc = reinterpret_cast<float*>(ws + off_dv);
-  std::vector<const void*> host(n_it * 11 * nb);
-  a.host_ptrs = host.data();
-  a.dev_ptrs = reinterpret_cast<void**>(ws + off_ptr);
-  int rc = da::run_backward(a, h, st);
-  if (rc >= 1000) return fail(DA_ERR_CUDA, "cuBLAS error %d in backward", rc - 1000);
-  if (rc) return fail(DA_ERR_CUDA, "CUDA error in backward: %s", cudaGetErrorString((cudaError_t)rc));
-  // the pageable pointer table must outlive the async upload
-  DA_CUDA(cudaStreamSynchronize(st));
-  g_last_launches = -1;  // kernels + cuBLAS calls (not counted)
-  return DA_OK;
+  return backward_fused(q, k, v, o, dout, lse, dq, dk, dv, p, P, st);
 }
 
 // ---------------------------------------------------------------------------- host entry point
@@ -887,6 +830,37 @@ int distr_attn_plan(int N, int d, int block_l, int group_size, int distr, da_pla
   return DA_OK;
 }
 
+// Cost-model constants (clk on one SM), measured on this build (tools/calibrate.sh, CTA-0
+// timelines at N = 16k, profiles/r02/calib.txt): steady clk per 128-key step of a CTA (two Q
+// tiles), and the CTA prologue (distr: Q landed + in-CTA hash + rank + Q̂ build + first S).
+struct StepCost {
+  int d, l, G;
+  double step, prologue;
+};
+constexpr StepCost kDistrCost[] = {
+    {64, 64, 2, 3169, 13342},  {64, 128, 2, 3100, 11030}, {64, 128, 4, 3190, 11367},
+    {64, 256, 2, 3045, 14314}, {64, 256, 4, 3112, 16459}, {128, 64, 2, 4625, 27688},
+    {128, 128, 2, 3190, 19609}, {128, 128, 4, 3252, 19108}, {128, 256, 2, 3153, 23418},
+    {128, 256, 4, 3167, 22970},
+};
+constexpr double kExactStep64 = 3268, kExactStep128 = 3356, kExactPrologue = 6000;
+
+// Predicted kernel time (us) of one flavour: CTAs (Q tile pairs) list-scheduled over 148 SMs.
+double predict_attn_us(int BH, int N, int causal, double step, double prologue, double mhz) {
+  const int nqt = (N + 127) / 128, npairs = (nqt + 1) / 2, nkt = nqt;
+  double total = 0, longest = 0;
+  for (int p = 0; p < npairs; ++p) {
+    const int steps = causal ? std::min(2 * p + 2, nkt) : nkt;
+    const double t = prologue + steps * step;
+    total += t;
+    longest = std::max(longest, t);
+  }
+  total *= BH;
+  const double sms = 148.0;
+  const double clk = std::max(total / sms, longest) + std::ceil(BH * (double)npairs / sms) * 400.0;
+  return clk / mhz;
+}
+
 const char* distr_attn_status_string(int status) {
   switch (status) {
     case DA_OK: return "ok";
@@ -895,6 +869,41 @@ const char* distr_attn_status_string(int status) {
     case DA_ERR_CUDA: return "CUDA error";
     default: return "unknown status";
   }
+}
+
+int distr_attn_choose(int B, int H, int H_kv, int N, int d, int causal, int max_group_size, double clk_mhz,
+                      da_choice* out) {
+  g_last_error.clear();
+  if (!out) return fail(DA_ERR_INVALID, "out is NULL");
+  if (B <= 0 || H <= 0 || H_kv <= 0 || N <= 0 || H % H_kv) return fail(DA_ERR_INVALID, "bad shape");
+  if (d != 32 && d != 64 && d != 128) return fail(DA_ERR_PRECONDITION, "d=%d unsupported", d);
+  const double mhz = clk_mhz > 0 ? clk_mhz : 1800.0;
+  const int BH = B * H;
+  const double launch_us = 4.0;
+  const double dc = d == 128 ? 128 : 64;  // d = 32 runs the d = 64 schedule (fewer K-steps, same softmax)
+  *out = da_choice{};
+  out->predicted_exact_us =
+      launch_us + predict_attn_us(BH, N, causal, dc == 128 ? kExactStep128 : kExactStep64, kExactPrologue, mhz);
+  // K^T layout pass: read K + write K^T (HBM, ~5.1 TB/s measured) + its launch
+  const double kt_us = launch_us + 2.0 * 2.0 * B * H_kv * (double)N * d / 5.1e6;
+  out->predicted_distr_us = 1e300;
+  for (const StepCost& c : kDistrCost) {
+    if (c.d != (int)dc || c.G > max_group_size) continue;
+    if (d / c.G < 16) continue;
+    const double t = launch_us + kt_us + predict_attn_us(BH, N, causal, c.step, c.prologue, mhz);
+    if (t < out->predicted_distr_us) {
+      out->predicted_distr_us = t;
+      out->block_l = c.l;
+      out->group_size = c.G;
+    }
+  }
+  out->distr = out->predicted_distr_us < out->predicted_exact_us;
+  out->predicted_us = out->distr ? out->predicted_distr_us : out->predicted_exact_us;
+  if (!out->distr) {
+    out->block_l = 0;
+    out->group_size = 1;
+  }
+  return DA_OK;
 }
 
 const char* distr_attn_last_error(void) { return g_last_error.c_str(); }

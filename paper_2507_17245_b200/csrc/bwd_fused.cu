@@ -19,8 +19,8 @@
 //    dQ̃ (fp32) goes to a workspace; fold_all_kernel (bwd.cu) folds it onto the representatives.
 //
 // Every operand layout and descriptor is the one the forward kernel (attn.cu) uses: natural
-// [rows][d] tiles in 64-column SWIZZLE_128B boxes serve as K-major operands (rows = M or N,
-// d = K) and as MN-major B operands (rows = K, d = N). d in {64, 128}.
+// [rows][d] tiles in RB-column SWIZZLE_{2 RB}B boxes (RB = 64, or 32 for d = 32) serve as K-major
+// operands (rows = M or N, d = K) and as MN-major B operands (rows = K, d = N). d in {32, 64, 128}.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -32,7 +32,6 @@ namespace {
 
 constexpr int T = 128;            // rows per tile (queries or keys)
 constexpr int kThreadsB = 384;    // warp 0 TMA, warp 1 MMA, warps 4..11 elementwise
-constexpr uint32_t kSw = kSw128;
 
 enum { BB_KV = 0, BB_FULL = 1, BB_EMPTY = 3, BB_SFULL = 5, BB_PFULL = 6, BB_DONE = 7, BB_TMEM = 8, BB_N = 9 };
 
@@ -46,15 +45,32 @@ struct BCfg {
   static constexpr int Q_SMEM = 2 * TILE + 2 * (2 * TILE) + 256 + 1024;
 };
 
+// Natural [128][d] tiles: boxes of RB columns (RB * 2-byte rows), swizzled SWIZZLE_{2 RB}B.
+template <int D>
+struct Box {
+  static constexpr int RB = D >= 64 ? 64 : D;
+  static constexpr int ROW = RB * 2;  // bytes per row inside a box
+  static constexpr uint32_t SW = RB == 64 ? kSw128 : kSw64;
+};
+template <int D>
 DA_DEV uint64_t kmaj(uint32_t base, int kk) {  // K-major operand of a [128][d] tile: K-step kk
-  return make_sdesc(base + (kk / 4) * (T * 128) + (kk % 4) * 32, 16, 1024, kSw);
+  using B = Box<D>;
+  constexpr int kpb = B::RB / 16;  // K-steps per box
+  return make_sdesc(base + (kk / kpb) * (T * B::ROW) + (kk % kpb) * 32, 16, 8 * B::ROW, B::SW);
 }
+template <int D>
 DA_DEV uint64_t mnmaj(uint32_t base, int kk) {  // MN-major B operand: 16 K-rows per step
-  return make_sdesc(base + kk * 2048, T * 128, 1024, kSw);
+  using B = Box<D>;
+  return make_sdesc(base + kk * 16 * B::ROW, T * B::ROW, 8 * B::ROW, B::SW);
 }
-DA_DEV void load_tile(uint8_t* dst, const CUtensorMap* m, uint64_t* bar, int D, int row, int plane) {
-  for (int bx = 0; bx < D / 64; ++bx) tma_load_3d(dst + bx * (T * 128), m, bar, bx * 64, row, plane);
+template <int D>
+DA_DEV void load_tile(uint8_t* dst, const CUtensorMap* m, uint64_t* bar, int row, int plane) {
+  using B = Box<D>;
+  for (int bx = 0; bx < D / B::RB; ++bx) tma_load_3d(dst + bx * (T * B::ROW), m, bar, bx * B::RB, row, plane);
 }
+// Epilogue helper: this thread's `cols` = D/2 consecutive fp32 TMEM columns in chunks of NC.
+template <int D>
+constexpr int epi_nc() { return D / 2 >= 32 ? 32 : D / 2; }
 
 // ------------------------------------------------------------------------------------ dK, dV
 template <int D>
@@ -63,6 +79,7 @@ __global__ void __launch_bounds__(kThreadsB, 1)
                   const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                   const BwdFusedArgs a) {
   using C = BCfg<D>;
+  constexpr int NC = epi_nc<D>();  // epilogue TMEM columns per load
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   uint8_t* sK = smem;
@@ -105,8 +122,8 @@ __global__ void __launch_bounds__(kThreadsB, 1)
   if (warp == 0) {
     if (lane == 0) {
       mbar_arrive_expect_tx(&bars[BB_KV], 2 * C::TILE);
-      load_tile(sK, &tmK, &bars[BB_KV], D, kt * T, bhkv);
-      load_tile(sV, &tmV, &bars[BB_KV], D, kt * T, bhkv);
+      load_tile<D>(sK, &tmK, &bars[BB_KV], kt * T, bhkv);
+      load_tile<D>(sV, &tmV, &bars[BB_KV], kt * T, bhkv);
       for (int n = 0; n < ntiles; ++n) {
         const int s = n & 1;
         int bh, qt;
@@ -114,8 +131,8 @@ __global__ void __launch_bounds__(kThreadsB, 1)
         mbar_wait(&bars[BB_EMPTY + s], ((n >> 1) & 1) ^ 1);
         uint8_t* st = ring + s * (2 * C::TILE + C::VEC);
         mbar_arrive_expect_tx(&bars[BB_FULL + s], 2 * C::TILE + C::VEC);
-        load_tile(st, &tmQt, &bars[BB_FULL + s], D, qt * T, bh);
-        load_tile(st + C::TILE, &tmdO, &bars[BB_FULL + s], D, qt * T, bh);
+        load_tile<D>(st, &tmQt, &bars[BB_FULL + s], qt * T, bh);
+        load_tile<D>(st + C::TILE, &tmdO, &bars[BB_FULL + s], qt * T, bh);
         bulk_g2s(st + 2 * C::TILE, a.lse_pad + ((size_t)bh * a.N_pad + qt * T), 512, &bars[BB_FULL + s]);
         bulk_g2s(st + 2 * C::TILE + 512, a.D_pad + ((size_t)bh * a.N_pad + qt * T), 512, &bars[BB_FULL + s]);
       }
@@ -133,9 +150,9 @@ __global__ void __launch_bounds__(kThreadsB, 1)
         tc_fence_after();
         const uint32_t qb = smem_u32(ring + s * (2 * C::TILE + C::VEC)), ob = qb + C::TILE;
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) mma_ss(tmem, kmaj(kb, kk), kmaj(qb, kk), IS, kk > 0);
+        for (int kk = 0; kk < D / 16; ++kk) mma_ss(tmem, kmaj<D>(kb, kk), kmaj<D>(qb, kk), IS, kk > 0);
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) mma_ss(tmem + 128, kmaj(vb, kk), kmaj(ob, kk), IS, kk > 0);
+        for (int kk = 0; kk < D / 16; ++kk) mma_ss(tmem + 128, kmaj<D>(vb, kk), kmaj<D>(ob, kk), IS, kk > 0);
         mma_commit(&bars[BB_SFULL]);
         mbar_wait(&bars[BB_PFULL], n & 1);
         tc_fence_after();
@@ -143,8 +160,8 @@ __global__ void __launch_bounds__(kThreadsB, 1)
         for (int kk = 0; kk < T / 16; ++kk) {
           // Pᵀ / dŜᵀ of queries [64h, 64h + 64) live in columns [64h, 64h + 32) of the Sᵀ / dPᵀ range
           const uint32_t pc = (uint32_t)((kk >> 2) * 64 + (kk & 3) * 8);
-          mma_ts(tmem + 256, tmem + pc, mnmaj(ob, kk), IG, (n > 0 || kk > 0) ? 1u : 0u);
-          mma_ts(tmem + 384, tmem + 128 + pc, mnmaj(qb, kk), IG, (n > 0 || kk > 0) ? 1u : 0u);
+          mma_ts(tmem + 256, tmem + pc, mnmaj<D>(ob, kk), IG, (n > 0 || kk > 0) ? 1u : 0u);
+          mma_ts(tmem + 384, tmem + 128 + pc, mnmaj<D>(qb, kk), IG, (n > 0 || kk > 0) ? 1u : 0u);
         }
         mma_commit(&bars[BB_EMPTY + s]);
       }
@@ -203,14 +220,14 @@ __global__ void __launch_bounds__(kThreadsB, 1)
       uint16_t* dst = (which == 0 ? a.dv : a.dk) + ((size_t)bhkv * a.N + key) * D + half * (D / 2);
       const uint32_t src = tmem + lb + (which == 0 ? 256 : 384) + half * (D / 2);
 #pragma unroll
-      for (int c = 0; c < D / 64; ++c) {
-        uint32_t r[32];
-        tmem_ld32(src + 32 * c, r);
+      for (int c = 0; c < D / 2 / NC; ++c) {
+        uint32_t r[NC];
+        tmem_ldn<NC>(src + NC * c, r);
         tmem_ld_wait();
         if (key < a.N) {
-          uint4* o = reinterpret_cast<uint4*>(dst + 32 * c);
+          uint4* o = reinterpret_cast<uint4*>(dst + NC * c);
 #pragma unroll
-          for (int e = 0; e < 4; ++e)
+          for (int e = 0; e < NC / 8; ++e)
             o[e] = make_uint4(pack_bf16x2(__uint_as_float(r[8 * e]), __uint_as_float(r[8 * e + 1])),
                               pack_bf16x2(__uint_as_float(r[8 * e + 2]), __uint_as_float(r[8 * e + 3])),
                               pack_bf16x2(__uint_as_float(r[8 * e + 4]), __uint_as_float(r[8 * e + 5])),
@@ -234,6 +251,7 @@ __global__ void __launch_bounds__(kThreadsB, 1)
                  const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
                  const BwdFusedArgs a) {
   using C = BCfg<D>;
+  constexpr int NC = epi_nc<D>();  // epilogue TMEM columns per load
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
   uint8_t* sQ = smem;
@@ -269,15 +287,15 @@ __global__ void __launch_bounds__(kThreadsB, 1)
   if (warp == 0) {
     if (lane == 0) {
       mbar_arrive_expect_tx(&bars[BB_KV], 2 * C::TILE);
-      load_tile(sQ, &tmQt, &bars[BB_KV], D, qt * T, bh);
-      load_tile(sO, &tmdO, &bars[BB_KV], D, qt * T, bh);
+      load_tile<D>(sQ, &tmQt, &bars[BB_KV], qt * T, bh);
+      load_tile<D>(sO, &tmdO, &bars[BB_KV], qt * T, bh);
       for (int n = 0; n < ntiles; ++n) {
         const int s = n & 1;
         mbar_wait(&bars[BB_EMPTY + s], ((n >> 1) & 1) ^ 1);
         uint8_t* st = ring + s * (2 * C::TILE);
         mbar_arrive_expect_tx(&bars[BB_FULL + s], 2 * C::TILE);
-        load_tile(st, &tmK, &bars[BB_FULL + s], D, n * T, bhkv);
-        load_tile(st + C::TILE, &tmV, &bars[BB_FULL + s], D, n * T, bhkv);
+        load_tile<D>(st, &tmK, &bars[BB_FULL + s], n * T, bhkv);
+        load_tile<D>(st + C::TILE, &tmV, &bars[BB_FULL + s], n * T, bhkv);
       }
     }
   } else if (warp == 1) {
@@ -293,15 +311,15 @@ __global__ void __launch_bounds__(kThreadsB, 1)
         tc_fence_after();
         const uint32_t kb = smem_u32(ring + s * (2 * C::TILE)), vb = kb + C::TILE;
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) mma_ss(tmem, kmaj(qb, kk), kmaj(kb, kk), IS, kk > 0);
+        for (int kk = 0; kk < D / 16; ++kk) mma_ss(tmem, kmaj<D>(qb, kk), kmaj<D>(kb, kk), IS, kk > 0);
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) mma_ss(tmem + 128, kmaj(ob, kk), kmaj(vb, kk), IS, kk > 0);
+        for (int kk = 0; kk < D / 16; ++kk) mma_ss(tmem + 128, kmaj<D>(ob, kk), kmaj<D>(vb, kk), IS, kk > 0);
         mma_commit(&bars[BB_SFULL]);
         mbar_wait(&bars[BB_PFULL], n & 1);
         tc_fence_after();
 #pragma unroll
         for (int kk = 0; kk < T / 16; ++kk)
-          mma_ts(tmem + 256, tmem + (uint32_t)((kk >> 2) * 64 + (kk & 3) * 8), mnmaj(kb, kk), IG,
+          mma_ts(tmem + 256, tmem + (uint32_t)((kk >> 2) * 64 + (kk & 3) * 8), mnmaj<D>(kb, kk), IG,
                  (n > 0 || kk > 0) ? 1u : 0u);
         mma_commit(&bars[BB_EMPTY + s]);
       }
@@ -347,14 +365,14 @@ __global__ void __launch_bounds__(kThreadsB, 1)
     tc_fence_after();
     float* dst = a.dqt + ((size_t)bh * a.N + row) * D + half * (D / 2);
 #pragma unroll
-    for (int c = 0; c < D / 64; ++c) {
-      uint32_t r[32];
-      tmem_ld32(tmem + lb + 256 + half * (D / 2) + 32 * c, r);
+    for (int c = 0; c < D / 2 / NC; ++c) {
+      uint32_t r[NC];
+      tmem_ldn<NC>(tmem + lb + 256 + half * (D / 2) + NC * c, r);
       tmem_ld_wait();
       if (row < a.N) {
-        float4* o = reinterpret_cast<float4*>(dst + 32 * c);
+        float4* o = reinterpret_cast<float4*>(dst + NC * c);
 #pragma unroll
-        for (int e = 0; e < 8; ++e)
+        for (int e = 0; e < NC / 4; ++e)
           o[e] = make_float4(__uint_as_float(r[4 * e]), __uint_as_float(r[4 * e + 1]), __uint_as_float(r[4 * e + 2]),
                              __uint_as_float(r[4 * e + 3]));
       }
@@ -386,6 +404,7 @@ cudaError_t launch_fused_t(const BwdFusedArgs& a, cudaStream_t st) {
 }  // namespace
 
 cudaError_t launch_bwd_fused(const BwdFusedArgs& a, cudaStream_t st) {
+  if (a.d == 32) return launch_fused_t<32>(a, st);
   if (a.d == 64) return launch_fused_t<64>(a, st);
   if (a.d == 128) return launch_fused_t<128>(a, st);
   return cudaErrorInvalidValue;

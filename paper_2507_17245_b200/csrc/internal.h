@@ -39,6 +39,8 @@ struct AttnArgs {
   int out_f32;
   float* lse;           // optional [BH][N]
   long long* trace;     // optional debug timeline of CTA (0,0): clock64() stamps, [20][256]
+  int pdl;              // launched as a programmatic dependent of the K^T prep kernel: the K
+                        // producer waits on the grid dependency before its first K^T load
 };
 
 cudaError_t launch_prep(const PrepArgs& a, cudaStream_t st);
@@ -58,29 +60,18 @@ struct GlobalArgs {
 };
 cudaError_t launch_global_prep(const GlobalArgs& a, cudaStream_t st);
 
-// Backward (bwd.cu). bf16 tensors [B*H or B*H_kv][N][d]; everything else workspace.
+// Backward helpers (bwd.cu). bf16 tensors [B*H][N][d]; everything else workspace.
 struct BwdArgs {
-  const uint16_t *q, *k, *v, *o, *dout;
-  const float* lse;       // [BH][N] natural-log sum-exp from the forward
+  const uint16_t *q, *o, *dout;
   const uint8_t* perm;    // [BH][nqb][d] (hash of q)
-  uint16_t *dq, *dk, *dv;  // outputs
-  int BH, BHkv, H, Hkv, N, d, G, nqb, block_l, causal;
-  float scale;
-  int R, nb;              // query rows per chunk, heads per batched GEMM
+  int BH, N, d, G, nqb, block_l;
   uint16_t* qt;           // [BH][N][d] Q̃
   float* D;               // [BH][Dstride]
-  int Dstride;            // N (cuBLAS path) or N_pad (fused path)
-  float *S, *dP;          // [nb][R][N] fp32
-  uint16_t *P16, *dS16;   // [nb][R][N] bf16
-  float* dqt;             // [nb][R][d]
-  float *dk_acc, *dv_acc; // [BH][N][d] fp32
-  const void** host_ptrs; // host staging for the batched-GEMM pointer arrays
-  void** dev_ptrs;        // device copy
+  int Dstride;            // N_pad (whole 128-row tiles)
 };
-int run_backward(const BwdArgs& a, void* cublas_handle, cudaStream_t st);  // 0 = ok
 
-// Fused tcgen05 backward (bwd_fused.cu), d in {64, 128}. Maps: Q̃, dO [BH][N][d]; K, V
-// [BHkv][N][d], all 64-column SWIZZLE_128B boxes of 128 rows.
+// Fused tcgen05 backward (bwd_fused.cu), d in {32, 64, 128}. Maps: Q̃, dO [BH][N][d]; K, V
+// [BHkv][N][d], all min(d, 64)-column SWIZZLE_{2 min(d, 64)}B boxes of 128 rows.
 struct BwdFusedArgs {
   const CUtensorMap *tmQt, *tmdO, *tmK, *tmV;
   const float* lse_pad;  // [BH][N_pad] (+inf past N)

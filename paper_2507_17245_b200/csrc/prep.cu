@@ -219,6 +219,10 @@ DA_DEV void kt_cta(const PrepArgs& a, int it, uint8_t* smem) {
 template <typename T, int D>
 __global__ void __launch_bounds__(kThreads) prep_kernel(const PrepArgs a) {
   extern __shared__ __align__(16) uint8_t smem[];
+  // Programmatic dependent launch: the attention kernel that follows may start its CTAs (and
+  // their in-CTA LSH prologue, which reads only Q) while this grid runs; it waits on the grid
+  // dependency before its first K^T load.
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int bid = blockIdx.x;
   if (bid < a.n_hash_ctas)
     hash_cta<T, D>(a, bid, smem);

@@ -31,7 +31,7 @@ def header_functions():
 
 def test_exports_every_declared_symbol(L):
     names = header_functions()
-    assert len(names) == 17, names
+    assert len(names) == 18, names
     assert names == set(_native.EXPORTED)
     for n in names:
         assert hasattr(L, n), n
@@ -143,3 +143,12 @@ def test_binding_rejects_bad_exports_and_lse():
                         bucket_ids=torch.zeros((1, 2, 2, 64), dtype=torch.int16),
                         perm=torch.zeros((1, 2, 2, 64), dtype=torch.uint8))
     assert ok.lse and ok.bucket_ids and ok.perm
+
+
+def test_library_has_no_cublas_dependency(L):
+    # every GEMM of the forward and backward runs in this library's tcgen05 kernels
+    import subprocess
+    deps = subprocess.run(["ldd", _native.LIB_PATH], capture_output=True, text=True).stdout
+    assert "cublas" not in deps.lower()
+    syms = subprocess.run(["nm", "-D", _native.LIB_PATH], capture_output=True, text=True).stdout
+    assert "cublas" not in syms.lower()

@@ -90,3 +90,53 @@ def test_plan_block256_shares_one_grouping_per_cta(d, g):
     assert p["smem_bytes"] <= 232448 and p["khat_stages"] >= 1
     # the paper's I/O model prefers the larger block
     assert p["hbm_bytes_paper"] < q["hbm_bytes_paper"]
+
+
+# ------------------------------------------------------------------------------ distr_attn_choose
+# The choosing planner against the measured sweeps committed under profiles/ (tools/sweep.py,
+# block_l 128 and 256, G* 2 and 4, and the own exact kernel): for every BASELINE config and C4
+# sweep point, the setting it picks must measure within 5 % of the fastest measured setting
+# (5 % = the run-to-run spread of these timings on one box).
+import glob
+import json
+import os
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+PROFILE = sorted(glob.glob(os.path.join(ROOT, "profiles", "r02_v*")))[-1]
+
+
+def measured():
+    rows = {}
+    for name in ("sweep.json", "sweep_l256.json"):
+        for line in open(os.path.join(PROFILE, name)):
+            r = json.loads(line)
+            key = (r["B"], r["H"], r["H_kv"], r["N"], r["d"], r["causal"], r["dtype"])
+            rows.setdefault(key, {})[("exact", 0, 1)] = min(
+                rows.get(key, {}).get(("exact", 0, 1), 1e9), r["exact_ms"])
+            rows[key][("distr", r["block_l"], r["G"])] = r["distr_ms"]
+    return rows
+
+
+@pytest.mark.parametrize("key", sorted(measured()))
+def test_choice_is_within_noise_of_the_fastest_measured(key):
+    B, H, Hkv, N, d, causal, dtype = key
+    cand = measured()[key]
+    c = da.distr_attn_choose(B, H, Hkv, N, d, causal=causal, max_group_size=4)
+    pick = ("distr", c["block_l"], c["group_size"]) if c["distr"] else ("exact", 0, 1)
+    if pick not in cand:  # a setting the sweep did not run at this shape (e.g. block_l=64)
+        pytest.skip(f"{pick} not measured at {key}")
+    best = min(cand.values())
+    assert cand[pick] <= 1.05 * best, (key, pick, cand)
+
+
+def test_choice_respects_the_accuracy_bound_and_envelope():
+    for N in (4096, 65536):
+        for mg in (1, 2, 4, 8):
+            c = da.distr_attn_choose(1, 16, 16, N, 128, max_group_size=mg)
+            assert c["group_size"] <= max(1, mg)
+            if mg == 1:
+                assert c["distr"] == 0  # G* = 1 is exact attention: nothing to gain
+            assert c["predicted_us"] == min(c["predicted_exact_us"], c["predicted_distr_us"])
+    assert da.distr_attn_choose(1, 1, 1, 4096, 32, max_group_size=8)["group_size"] <= 2  # d/G* >= 16
+    with pytest.raises(DistrAttnError):
+        da.distr_attn_choose(1, 3, 2, 128, 128)

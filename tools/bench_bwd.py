@@ -1,14 +1,13 @@
 """Backward timing (distr_attn_bwd_ex): CUDA events around the C call, after
-warm-up, on the C4 shape (B=1 H=16 d=128) at N in {4k, 16k}, G* in {1, 2}, for the fused tcgen05
-path (default) and the first cuBLAS version (DA_BWD_CUBLAS=1).
+warm-up, on the C4 shape (B=1 H=16) at N in {4k, 16k}, G* in {1, 2}, for the fused tcgen05
+kernels (d = 32, 64, 128; G* = 1, 2).
 
     python tools/bench_bwd.py > gpurun_out/bwd.json
 
 Algorithmic FLOP per call: five GEMMs of 2·N·N_k·d (Ŝ = Q̃Kᵀ, dP = dO Vᵀ, dV = Pᵀ dO, dQ̃ = dŜ K,
 dK = dŜᵀ Q̃) per head ("tflops_executed" counts these; the fused path runs seven MMAs per tile
 pair — Ŝ and dP in both of its kernels — so its tensor pipe does 7/5 of that). Roofline against
-MEASURED_PEAKS bf16. The cuBLAS path materialises the score tiles (S, dP fp32; P, dŜ bf16: 12 B per
-(query, key) pair, written and read back; "score_tile_bytes") and is bound by that traffic.
+MEASURED_PEAKS bf16.
 """
 import json, os, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -24,13 +23,10 @@ except Exception:
     pass
 peak = peaks.get("bf16_tflops_sustained", peaks.get("bf16_tflops", 2250.0))
 for N in (4096, 16384):
-  for path in ("fused", "cublas"):
-    if path == "cublas":
-        os.environ["DA_BWD_CUBLAS"] = "1"
-    else:
-        os.environ.pop("DA_BWD_CUBLAS", None)
+  for d in (32, 64, 128):
+    path = "fused"
     for G in (1, 2):
-        c = CONFIGS["C4"].with_(B=1, H=16, H_kv=16, N=N, group_size=G)
+        c = CONFIGS["C4"].with_(B=1, H=16, H_kv=16, N=N, d=d, group_size=G)
         q, k, v = make_qkv(c, device="cuda")
         dout = torch.randn_like(q.float()).bfloat16()
         lse = torch.empty(q.shape[:3], dtype=torch.float32, device="cuda")
@@ -47,8 +43,7 @@ for N in (4096, 16384):
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / steps
         flop = 5 * 2.0 * N * N * c.d * c.H
-        rec = {"path": path, "N": N, "G": G, "B": 1, "H": 16, "d": 128, "bwd_ms": ms,
+        rec = {"path": path, "N": N, "G": G, "B": 1, "H": 16, "d": d, "bwd_ms": ms,
                "tflops_executed": flop / (ms * 1e-3) / 1e12, "peak_tflops": peak,
-               "frac_of_peak": flop / (ms * 1e-3) / 1e12 / peak,
-               "score_tile_bytes": 12.0 * N * N * c.H * 2}
+               "frac_of_peak": flop / (ms * 1e-3) / 1e12 / peak}
         print(json.dumps(rec), flush=True)

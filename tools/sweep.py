@@ -18,6 +18,8 @@ ap.add_argument("--steps", type=int, default=10)
 ap.add_argument("--warmup", type=int, default=3)
 ap.add_argument("--only", default="", help="comma-separated case-name prefixes (default: all)")
 ap.add_argument("--block-l", type=int, default=0, help="override block_l of every case (e.g. 256)")
+ap.add_argument("--plan", action="store_true",
+                help="also run distr_attn_choose's pick for each case (max_group_size = the case's G*)")
 args = ap.parse_args()
 L = _native.lib()
 cases = [("C1", CONFIGS["C1"]), ("C2", CONFIGS["C2"]), ("C3", CONFIGS["C3"])]
@@ -30,18 +32,26 @@ if args.block_l:
 
 
 def timed(fn):
+    """(ms per call over `steps` back-to-back calls, attention-kernel ms). The call time is taken
+    with no per-call events armed (the K^T pass and the attention kernel may overlap through
+    programmatic dependent launch); the kernel split comes from a second pass with the events
+    recorded between the launches (which serialises them)."""
     for _ in range(args.warmup):
         fn(None)
+    torch.cuda.synchronize()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0.record()
+    for _ in range(args.steps):
+        fn(None)
+    t1.record()
+    torch.cuda.synchronize()
     evs = [[torch.cuda.Event(enable_timing=True) for _ in range(3)] for _ in range(args.steps)]
     for e3 in evs:
         for e in e3:
             e.record()
     torch.cuda.synchronize()
-    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    t0.record()
     for e3 in evs:
         fn(e3)
-    t1.record()
     torch.cuda.synchronize()
     attn = sum(e[1].elapsed_time(e[2]) for e in evs) / args.steps
     return t0.elapsed_time(t1) / args.steps, attn
@@ -70,6 +80,18 @@ for name, c in cases:
            "distr_tflops_executed": pairs * (2 * DR + 2 * c.d) / (d_attn * 1e-3) / 1e12,
            "exact_tflops": pairs * 4 * c.d / (x_attn * 1e-3) / 1e12,
            "full_d_equiv_tflops": pairs * 4 * c.d / (d_ms * 1e-3) / 1e12}
+    if args.plan:
+        ch = da.distr_attn_choose(c.B, c.H, c.H_kv, c.N, c.d, causal=c.causal, max_group_size=c.group_size)
+        if ch["distr"]:
+            def run_plan(evs):
+                if evs is not None:
+                    L.distr_attn_set_profile_events(*[ctypes.c_void_p(e.cuda_event) for e in evs])
+                da.distr_attn_fwd_ex(q, k, v, out, block_l=ch["block_l"], group_size=ch["group_size"],
+                                     causal=c.causal)
+            p_ms, _ = timed(run_plan)
+        else:
+            p_ms = x_ms
+        rec["plan"] = dict(ch, measured_ms=p_ms)
     print(json.dumps(rec), flush=True)
     del q, k, v, out
     torch.cuda.empty_cache()
