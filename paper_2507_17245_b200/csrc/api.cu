@@ -830,9 +830,12 @@ int distr_attn_plan(int N, int d, int block_l, int group_size, int distr, da_pla
   return DA_OK;
 }
 
-// Cost-model constants (clk on one SM), measured on this build (tools/calibrate.sh, CTA-0
-// timelines at N = 16k, profiles/r02/calib.txt): steady clk per 128-key step of a CTA (two Q
-// tiles), and the CTA prologue (distr: Q landed + in-CTA hash + rank + Q̂ build + first S).
+// Cost-model constants (clk on one SM), measured on this build: the CTA prologue (distr: Q landed
+// + in-CTA hash + rank + Q̂ build + first S) from CTA-0 timelines (tools/calibrate.sh,
+// profiles/r02_v1/calib.txt); the steady clk per 128-key step of a CTA (two Q tiles) for d = 128
+// from the long-sequence sweeps (N = 32k / 64k, where the prologue is < 2 % of the time: the
+// distr/exact time ratios of profiles/r02_v1 and r02_v2, averaged, times the exact kernel's
+// timeline step); d = 64 steps from the timelines.
 struct StepCost {
   int d, l, G;
   double step, prologue;
@@ -840,8 +843,8 @@ struct StepCost {
 constexpr StepCost kDistrCost[] = {
     {64, 64, 2, 3169, 13342},  {64, 128, 2, 3100, 11030}, {64, 128, 4, 3190, 11367},
     {64, 256, 2, 3045, 14314}, {64, 256, 4, 3112, 16459}, {128, 64, 2, 4625, 27688},
-    {128, 128, 2, 3190, 19609}, {128, 128, 4, 3252, 19108}, {128, 256, 2, 3153, 23418},
-    {128, 256, 4, 3167, 22970},
+    {128, 128, 2, 3088, 19609}, {128, 128, 4, 3004, 19108}, {128, 256, 2, 3088, 23418},
+    {128, 256, 4, 2953, 22970},
 };
 constexpr double kExactStep64 = 3268, kExactStep128 = 3356, kExactPrologue = 6000;
 
@@ -897,7 +900,9 @@ int distr_attn_choose(int B, int H, int H_kv, int N, int d, int causal, int max_
       out->group_size = c.G;
     }
   }
-  out->distr = out->predicted_distr_us < out->predicted_exact_us;
+  // the approximation is taken only when it is predicted clearly faster than exact attention
+  // (more accurate by definition): by more than the model's spread against the sweeps, 3 %
+  out->distr = out->predicted_distr_us < 0.97 * out->predicted_exact_us;
   out->predicted_us = out->distr ? out->predicted_distr_us : out->predicted_exact_us;
   if (!out->distr) {
     out->block_l = 0;
