@@ -221,11 +221,21 @@ def main():
     from paper_2507_17245_b200 import _native
 
     rank, world, local = dist_env()
+    # BENCH_SHARE_GPU=1 (tests only): every rank on cuda:0 with the gloo backend, so the
+    # multi-rank path (sharding, max-over-ranks timing, verification gather) runs on a 1-GPU box;
+    # NCCL refuses two ranks on one device. The driver's multi-GPU runs use NCCL, one GPU per rank.
+    share = os.environ.get("BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        if share:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
+    coll_dev = torch.device("cpu") if share else dev  # gloo collectives on host tensors
     from paper_2507_17245_b200.shard import (batch_shard, head_shard, make_head_shard, max_over_ranks,
                                              q_pair_shard, q_rows_of_shard)
     G = cfg.group_size
@@ -286,7 +296,7 @@ def main():
         attn = [e[1].elapsed_time(e[2]) for e in evs]
         prep = [e[0].elapsed_time(e[1]) for e in evs]
         per_step = [e[0].elapsed_time(e[2]) for e in evs]
-        total, a_ms, p_ms = max_over_ranks([total, np.mean(attn), np.mean(prep)], device=dev)
+        total, a_ms, p_ms = max_over_ranks([total, np.mean(attn), np.mean(prep)], device=coll_dev)
         return (total / args.steps, a_ms, p_ms, launches_per_step, clk.summary(),
                 {"step": pct(per_step), "attn_kernel": pct(attn)})
 
@@ -317,7 +327,6 @@ def main():
     if not args.no_parity:
         sys.path.insert(0, os.path.join(ROOT, "tests"))
         from gpu_util import errors, oracle_items, valid_rows_mask
-        from synth import sample_items
         step(False)
         torch.cuda.synchronize()
         nb_local = heads[1] - heads[0]
@@ -325,8 +334,8 @@ def main():
             own = q_rows_of_shard(cfg.N, rank, world, cfg.causal)
             local = [(0, own[0][0] // cfg.block_l)]
         else:
-            lc = cfg.with_(B=1, H=nb_local, H_kv=max(1, nb_local // (cfg.H // cfg.H_kv)))
-            local = sample_items(lc, n_heads=2, per_head=2, seed=7 + rank)
+            # the same number of items on every rank (all_gather needs equal shapes)
+            local = [(0, 0), (nb_local - 1, cfg.nqb - 1), (nb_local // 2, cfg.nqb // 2)]
         flat = out.reshape(-1, cfg.N, cfg.d)
         blk = torch.zeros((len(local), cfg.block_l, cfg.d), dtype=out.dtype, device=dev)
         for j, (bh, qb) in enumerate(local):
@@ -334,6 +343,7 @@ def main():
             blk[j, :r1 - r0] = flat[bh, r0:r1]
         idx = torch.tensor([[heads[0] + bh, qb] for bh, qb in local], dtype=torch.int64, device=dev)
         if world > 1:
+            blk, idx = blk.to(coll_dev), idx.to(coll_dev)
             blks = [torch.empty_like(blk) for _ in range(world)]
             idxs = [torch.empty_like(idx) for _ in range(world)]
             torch.distributed.all_gather(blks, blk)
@@ -382,7 +392,7 @@ def main():
             da.distr_attn_fwd_host(qh, kh, vh, oh, block_l=cfg.block_l, group_size=G, q_shard=qsh)
         e1.record(stream)
         barrier()
-        e_ms = max_over_ranks([e0.elapsed_time(e1) / n_e2e], device=dev)[0]
+        e_ms = max_over_ranks([e0.elapsed_time(e1) / n_e2e], device=coll_dev)[0]
         same = bool(torch.equal(oh, out.cpu())) if qsh is None else None
         nbytes = q.numel() * q.element_size()
         kvbytes = k.numel() * k.element_size()
