@@ -150,11 +150,11 @@ def oracle_sample_time(cfg, q, k, v, G, n_items, seed=0):
     return time.perf_counter() - t0, len(items), oracle.num_threads()
 
 
-def bench_config(cfg, G, B_per_rank, world, shard):
+def bench_config(cfg, G, heads_per_rank, world, shard):
     """The `config` object of the JSON line (identical for both arms)."""
     return {"workload": f"{cfg.name}: B={cfg.B} H={cfg.H} N={cfg.N} d={cfg.d} block_l={cfg.block_l} "
                         f"G*={G} bf16 {'causal' if cfg.causal else 'non-causal'}",
-            "B_per_rank": B_per_rank,
+            "heads_per_rank": heads_per_rank,
             "parallelism": (f"Q-tile-pair-sharded x{world}" if shard == "q" else f"(b,h)-sharded x{world}"),
             "l2": "inputs (17 GB) larger than L2, no flush"}
 
@@ -165,6 +165,9 @@ def run_reference(args, cfg):
     if rank != 0:
         return
     import oracle
+    # torchrun sets OMP_NUM_THREADS=1 for multi-process jobs; the reference arm (rank 0 alone)
+    # times the oracle on all of the box's host cores
+    oracle.set_num_threads(len(os.sched_getaffinity(0)))
     G = cfg.group_size
     B = cfg.B
     # one head's inputs on the host; each step = a bounded sample of Q blocks
@@ -185,7 +188,7 @@ def run_reference(args, cfg):
         "impl": "reference", "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-        "data": "synthetic", "config": bench_config(cfg, G, B, world, "bh"),
+        "data": "synthetic", "config": bench_config(cfg, G, cfg.B * cfg.H, world, "bh"),
         "cpu_baseline": {"value": ms, "unit": "ms", "cores": oracle.num_threads(),
                          "kind": "oracle", "sample": sample},
         "e2e": {"value": ms, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -419,7 +422,7 @@ def main():
             "metric": METRIC, "value": ms, "unit": "ms", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": False,
             "scaling": "strong", "vs_baseline": None, "dtype": "bf16", "data": "synthetic",
-            "config": bench_config(cfg, G, B_rank, world, args.shard),
+            "config": bench_config(cfg, G, int(heads[1] - heads[0]), world, args.shard),
             "exact_ms": ex_ms, "speedup_vs_exact": ex_ms / ms,
             "attn_kernel_ms": attn_ms, "prep_kernel_ms": prep_ms, "exact_kernel_ms": ex_attn_ms,
             "percentiles_ms": {"distr": dist_ms, "exact": ex_dist},
