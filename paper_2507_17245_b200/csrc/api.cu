@@ -400,10 +400,11 @@ int forward(const void* q, const void* k, const void* v, void* out, const da_par
   return DA_OK;
 }
 
-// Workspace of the global-grouping variant: perm [BH][d] u8, Q̂ and K̂ [BH][N][d/G*] bf16.
+// Workspace of the global-grouping variant: perm [BH][d] u8, sign patterns [BH][d] u16, Q̂ and K̂
+// [BH][N][d/G*] bf16.
 size_t global_ws_bytes(const Plan& P, size_t* off_qhat, size_t* off_khat) {
   const size_t BH = (size_t)P.B * P.H, DR = (size_t)P.d / P.G;
-  size_t o = al256(BH * P.d);
+  size_t o = al256(BH * P.d) + al256(BH * P.d * 2);
   *off_qhat = o;
   o = al256(o + BH * P.N * DR * 2);
   *off_khat = o;
@@ -443,6 +444,7 @@ int forward_global(const void* q, const void* k, const void* v, void* out, const
   g.BH = (int)BH; g.H = P.H; g.Hkv = P.Hkv; g.N = P.N; g.d = P.d; g.G = P.G;
   g.proj = proj;
   g.perm = ws;
+  g.gpat = reinterpret_cast<uint16_t*>(ws + al256(BH * P.d));
   g.bucket_out = p->bucket_ids;
   g.perm_out = p->perm;
   g.qhat = reinterpret_cast<uint16_t*>(ws + off_qh);

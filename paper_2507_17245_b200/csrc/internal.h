@@ -52,6 +52,7 @@ struct GlobalArgs {
   const uint16_t* k;     // [BHkv][N][d]
   int BH, H, Hkv, N, d, G;
   const float* proj;     // [16][N] (seed, N)
+  uint16_t* gpat;        // [BH][d] workspace: 16-bit sign pattern per column
   uint8_t* perm;         // [BH][d] workspace
   uint16_t* bucket_out;  // optional export [BH][d]
   uint8_t* perm_out;     // optional export [BH][d]

@@ -6,11 +6,12 @@
 // Reading R17: the global variant is block-wise DistrAttention with one hash block of height N
 // (projection matrix 16 x N from (seed, N)); the oracle computes it with block_l = N.
 //
-// global_hash_kernel, one CTA per (b*H + h), 256 threads: y[k][c] = sum_{r < N} P[k][r] Q[r][c]
-//   as ONE fp32 fma chain in ascending r from +0.0f (the bit-exact contract of R6, now over N
-//   rows), streamed through shared memory 128 rows at a time with the next chunk's global loads
-//   in flight; then bits -> inverse Gray -> stable rank by (bucket, column) -> perm[bh][d].
-// global_gather_kernel, one CTA per (b*H + h, 64 rows): Q̂[r][j] = Q[r][perm[jG]] and
+// global_hash_kernel, one CTA per (b*H + h, 16 columns), 128 threads: y[k][c] = sum_{r < N}
+//   P[k][r] Q[r][c] as ONE fp32 fma chain in ascending r from +0.0f (the bit-exact contract of R6,
+//   now over N rows), streamed through shared memory 128 rows at a time with the next chunk's
+//   global loads in flight -> 16-bit sign patterns gpat[bh][c].
+// global_gather_kernel, one CTA per (b*H + h, 64 rows): patterns -> inverse Gray -> stable rank by
+//   (bucket, column) -> perm (CTA 0 of the head writes perm and the exports); Q̂[r][j] = Q[r][perm[jG]] and
 //   K̂[r][j] = bf16(sum_g K_kv[r][perm[jG+g]]) (fp32 sum in group order, one rounding: R15),
 //   both [BH][N][DR] bf16 with DR = d/G* — K̂ per QUERY head (GQA heads of one KV head have
 //   different groupings).
@@ -36,41 +37,39 @@ DA_DEV uint32_t inverse_gray16g(uint32_t p) {
   return p & 0xFFFFu;
 }
 
+// One CTA per (b*H + h, 16-column slice): thread = (column c of the slice, projection-row pair
+// kq), ONE fp32x2 fma chain over all N rows in ascending order (the R6 contract) — 2048 chains
+// per head at d = 128 spread over d/16 CTAs, so a handful of heads (C4: 16) still fills the GPU.
+// Rows are staged through shared memory 128 at a time with the next chunk's global loads in
+// flight. Output: the 16-bit sign pattern of each column (gpat[bh][c]); the gather kernel turns the
+// patterns into buckets and the permutation.
+constexpr int kHT = 128;   // hash threads: 16 columns x 8 projection-row pairs
+constexpr int kHC = 16;    // columns per hash CTA
 template <int D>
-__global__ void __launch_bounds__(kT) global_hash_kernel(const GlobalArgs a) {
-  constexpr int QP = D + 8;              // staged row pitch (bf16): 16-byte rows, bank spread
-  constexpr int VPR = D / 8;             // 16-byte vectors per row
-  constexpr int NIT = kChunk * VPR / kT;  // vectors per thread per chunk
-  __shared__ __align__(16) uint16_t q_s[kChunk * QP];
-  __shared__ __align__(16) float proj_t[kChunk * 16];  // [r][16]
-  __shared__ uint32_t pat_s[kT];  // [NKG][D]
-  __shared__ uint32_t key_s[D];
-  __shared__ uint8_t perm_s[D];
-  const int bh = blockIdx.x;
-  const uint16_t* qg = a.q + (size_t)bh * a.N * D;
+__global__ void __launch_bounds__(kHT) global_hash_kernel(const GlobalArgs a) {
+  __shared__ __align__(16) uint32_t q_s[kChunk * kHC / 2];  // [r][16 columns] bf16 pairs
+  __shared__ __align__(16) float proj_t[kChunk * 16];      // [r][16]
+  __shared__ uint32_t bits_s[8][kHC];
+  const int bh = blockIdx.x, c0 = blockIdx.y * kHC;
+  const int cl = threadIdx.x % kHC, kq = threadIdx.x / kHC;  // column of the slice, rows 2kq, 2kq+1
+  const uint16_t* qg = a.q + (size_t)bh * a.N * D + c0;
   const int nchunk = (a.N + kChunk - 1) / kChunk;
-
-  constexpr int NKG = kT / D;  // projection-row groups: 2 (d=128), 4 (d=64) or 8 (d=32)
-  constexpr int KPT = 16 / NKG;
-  const int c = threadIdx.x % D, kg = threadIdx.x / D, k0 = kg * KPT;
-  float2 y[KPT / 2];
-#pragma unroll
-  for (int m = 0; m < KPT / 2; ++m) y[m] = make_float2(0.0f, 0.0f);
-
-  uint4 nxt[NIT];
-  float pnx[kChunk * 16 / kT];
+  float2 y = make_float2(0.0f, 0.0f);
+  // staging per chunk: 128 rows x 16 columns bf16 = 256 16-byte vectors (2 per thread) and the
+  // projection [16][128 rows] (16 per thread)
+  uint4 nq[2];
+  float np_[16];
   auto load_chunk = [&](int ci) {
     const int r0 = ci * kChunk, rows = min(kChunk, a.N - r0);
 #pragma unroll
-    for (int u = 0; u < NIT; ++u) {
-      const int i = threadIdx.x + u * kT;
-      nxt[u] = i < rows * VPR ? reinterpret_cast<const uint4*>(qg + (size_t)r0 * D)[i] : make_uint4(0, 0, 0, 0);
+    for (int u = 0; u < 2; ++u) {
+      const int i = threadIdx.x + u * kHT, r = i >> 1, half = i & 1;  // 2 vectors per row
+      nq[u] = r < rows ? *reinterpret_cast<const uint4*>(qg + (size_t)(r0 + r) * D + half * 8) : make_uint4(0, 0, 0, 0);
     }
 #pragma unroll
-    for (int u = 0; u < kChunk * 16 / kT; ++u) {
-      const int i = threadIdx.x + u * kT;  // (k, r) = (i / kChunk, i % kChunk): coalesced in r
-      const int k = i / kChunk, r = i % kChunk;
-      pnx[u] = r < rows ? a.proj[(size_t)k * a.N + r0 + r] : 0.0f;
+    for (int u = 0; u < 16; ++u) {
+      const int i = threadIdx.x + u * kHT, k = i / kChunk, r = i % kChunk;  // coalesced in r
+      np_[u] = r < rows ? a.proj[(size_t)k * a.N + r0 + r] : 0.0f;
     }
   };
   load_chunk(0);
@@ -78,60 +77,28 @@ __global__ void __launch_bounds__(kT) global_hash_kernel(const GlobalArgs a) {
     const int rows = min(kChunk, a.N - ci * kChunk);
     __syncthreads();  // previous chunk consumed
 #pragma unroll
-    for (int u = 0; u < NIT; ++u) {
-      const int i = threadIdx.x + u * kT;
-      *reinterpret_cast<uint4*>(q_s + (i / VPR) * QP + (i % VPR) * 8) = nxt[u];
-    }
+    for (int u = 0; u < 2; ++u) reinterpret_cast<uint4*>(q_s)[threadIdx.x + u * kHT] = nq[u];
 #pragma unroll
-    for (int u = 0; u < kChunk * 16 / kT; ++u) {
-      const int i = threadIdx.x + u * kT;
-      proj_t[(i % kChunk) * 16 + i / kChunk] = pnx[u];
+    for (int u = 0; u < 16; ++u) {
+      const int i = threadIdx.x + u * kHT;
+      proj_t[(i % kChunk) * 16 + i / kChunk] = np_[u];
     }
     __syncthreads();
     if (ci + 1 < nchunk) load_chunk(ci + 1);  // next chunk's loads fly under this chunk's FMAs
-    for (int r = 0; r < rows; ++r) {
-      const float qv = __uint_as_float(((uint32_t)q_s[r * QP + c]) << 16);
-      const float2 qq = make_float2(qv, qv);
-      if constexpr (KPT == 2) {
-        y[0] = fma2(*reinterpret_cast<const float2*>(proj_t + r * 16 + k0), qq, y[0]);
-      } else {
-#pragma unroll
-        for (int m = 0; m < KPT / 4; ++m) {
-          const float4 pa = *reinterpret_cast<const float4*>(proj_t + r * 16 + k0 + 4 * m);
-          y[2 * m] = fma2(make_float2(pa.x, pa.y), qq, y[2 * m]);
-          y[2 * m + 1] = fma2(make_float2(pa.z, pa.w), qq, y[2 * m + 1]);
-        }
-      }
+    const uint16_t* qc = reinterpret_cast<const uint16_t*>(q_s);
+#pragma unroll 8
+    for (int r = 0; r < rows; ++r) {  // ascending rows: the R6 fp32 fma chain
+      const float qv = __uint_as_float(((uint32_t)qc[r * kHC + cl]) << 16);
+      y = fma2(*reinterpret_cast<const float2*>(proj_t + r * 16 + 2 * kq), make_float2(qv, qv), y);
     }
   }
-  uint32_t part = 0;
-#pragma unroll
-  for (int m = 0; m < KPT / 2; ++m) {
-    part |= (y[m].x > 0.0f ? 1u : 0u) << (k0 + 2 * m);
-    part |= (y[m].y > 0.0f ? 1u : 0u) << (k0 + 2 * m + 1);
-  }
-  pat_s[kg * D + c] = part;
+  bits_s[kq][cl] = (y.x > 0.0f ? 1u : 0u) << (2 * kq) | (y.y > 0.0f ? 1u : 0u) << (2 * kq + 1);
   __syncthreads();
-  if (threadIdx.x < D) {
+  if (threadIdx.x < kHC) {
     uint32_t pattern = 0;
 #pragma unroll
-    for (int g = 0; g < NKG; ++g) pattern |= pat_s[g * D + threadIdx.x];
-    const uint32_t bucket = inverse_gray16g(pattern);
-    key_s[threadIdx.x] = (bucket << 8) | (uint32_t)threadIdx.x;  // unique (bucket, column) key
-    if (a.bucket_out) a.bucket_out[(size_t)bh * D + threadIdx.x] = (uint16_t)bucket;
-  }
-  __syncthreads();
-  if (threadIdx.x < D) {
-    const uint32_t mine = key_s[threadIdx.x];
-    int rank = 0;
-#pragma unroll 16
-    for (int j = 0; j < D; ++j) rank += key_s[j] < mine ? 1 : 0;
-    perm_s[rank] = (uint8_t)threadIdx.x;
-  }
-  __syncthreads();
-  if (threadIdx.x < D) {
-    a.perm[(size_t)bh * D + threadIdx.x] = perm_s[threadIdx.x];
-    if (a.perm_out) a.perm_out[(size_t)bh * D + threadIdx.x] = perm_s[threadIdx.x];
+    for (int g = 0; g < 8; ++g) pattern |= bits_s[g][threadIdx.x];
+    a.gpat[(size_t)bh * D + c0 + threadIdx.x] = (uint16_t)pattern;
   }
 }
 
@@ -144,9 +111,29 @@ __global__ void __launch_bounds__(kT) global_gather_kernel(const GlobalArgs a) {
   __shared__ __align__(16) uint16_t q_s[R * QP];
   __shared__ __align__(16) uint16_t k_s[R * QP];
   __shared__ uint8_t perm_s[D];
+  __shared__ uint32_t key_s[D];
   const int bh = blockIdx.y, r0 = blockIdx.x * R, rows = min(R, a.N - r0);
   const int b = bh / a.H, h = bh % a.H, bhkv = b * a.Hkv + h / (a.H / a.Hkv);
-  if (threadIdx.x < D) perm_s[threadIdx.x] = a.perm[(size_t)bh * D + threadIdx.x];
+  // buckets (inverse Gray of the sign pattern) and the stable rank by (bucket, column): the same
+  // few thousand compares in every CTA of the head; CTA 0 writes the perm and the exports
+  if (threadIdx.x < D) {
+    const uint32_t bucket = inverse_gray16g(a.gpat[(size_t)bh * D + threadIdx.x]);
+    key_s[threadIdx.x] = (bucket << 8) | (uint32_t)threadIdx.x;  // unique (bucket, column) key
+    if (blockIdx.x == 0 && a.bucket_out) a.bucket_out[(size_t)bh * D + threadIdx.x] = (uint16_t)bucket;
+  }
+  __syncthreads();
+  if (threadIdx.x < D) {
+    const uint32_t mine = key_s[threadIdx.x];
+    int rank = 0;
+#pragma unroll 16
+    for (int j = 0; j < D; ++j) rank += key_s[j] < mine ? 1 : 0;
+    perm_s[rank] = (uint8_t)threadIdx.x;
+  }
+  __syncthreads();
+  if (blockIdx.x == 0 && threadIdx.x < D) {
+    a.perm[(size_t)bh * D + threadIdx.x] = perm_s[threadIdx.x];
+    if (a.perm_out) a.perm_out[(size_t)bh * D + threadIdx.x] = perm_s[threadIdx.x];
+  }
   const uint4* qg = reinterpret_cast<const uint4*>(a.q + ((size_t)bh * a.N + r0) * D);
   const uint4* kg = reinterpret_cast<const uint4*>(a.k + ((size_t)bhkv * a.N + r0) * D);
   constexpr int NIT = R * VPR / kT;
@@ -193,12 +180,13 @@ __global__ void __launch_bounds__(kT) global_gather_kernel(const GlobalArgs a) {
 }  // namespace
 
 cudaError_t launch_global_prep(const GlobalArgs& a, cudaStream_t st) {
+  const dim3 hgrid(a.BH, a.d / kHC);
   if (a.d == 32)
-    global_hash_kernel<32><<<a.BH, kT, 0, st>>>(a);
+    global_hash_kernel<32><<<hgrid, kHT, 0, st>>>(a);
   else if (a.d == 64)
-    global_hash_kernel<64><<<a.BH, kT, 0, st>>>(a);
+    global_hash_kernel<64><<<hgrid, kHT, 0, st>>>(a);
   else
-    global_hash_kernel<128><<<a.BH, kT, 0, st>>>(a);
+    global_hash_kernel<128><<<hgrid, kHT, 0, st>>>(a);
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return e;
   const dim3 grid((a.N + 63) / 64, a.BH);

@@ -99,8 +99,9 @@ def test_workspace_size_formula(L):
     p = params(B=2, H=4, N=1000, d=128, block_l=128, G=2)
     BH, nqb, N_pad = 8, 8, 1000
     al = lambda x: (x + 255) // 256 * 256
-    # ... or, when larger, the global-grouping variant's perm [BH][d] + Q̂ and K̂ [BH][N][d/G*]
-    glob = al(BH * 128) + 2 * al(BH * 1000 * 64 * 2)
+    # ... or, when larger, the global-grouping variant: perm [BH][d] u8 + sign patterns [BH][d] u16
+    # + Q̂ and K̂ [BH][N][d/G*]
+    glob = al(BH * 128) + al(BH * 128 * 2) + 2 * al(BH * 1000 * 64 * 2)
     assert L.distr_attn_workspace_size(ctypes.byref(p)) == max(al(BH * 128 * N_pad * 2), glob)
     # distr, fp32: perm [BH][nqb][d] + K^T + bf16 copies of Q and V
     p = params(B=2, H=4, N=1000, d=128, block_l=128, G=2, dtype=1)
