@@ -138,24 +138,28 @@ __global__ void __launch_bounds__(kThreadsB, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t IS = make_idesc_bf16(T, T, false, false);   // Sᵀ, dPᵀ
-      constexpr uint32_t IG = make_idesc_bf16(T, D, false, true);    // dV, dK (B MN-major)
-      mbar_wait(&bars[BB_KV], 0);
+    // whole warp runs the loop (uniform descriptors), one elected lane issues each batch
+    constexpr uint32_t IS = make_idesc_bf16(T, T, false, false);   // Sᵀ, dPᵀ
+    constexpr uint32_t IG = make_idesc_bf16(T, D, false, true);    // dV, dK (B MN-major)
+    mbar_wait(&bars[BB_KV], 0);
+    tc_fence_after();
+    const uint32_t kb = smem_u32(sK), vb = smem_u32(sV);
+    for (int n = 0; n < ntiles; ++n) {
+      const int s = n & 1;
+      mbar_wait(&bars[BB_FULL + s], (n >> 1) & 1);
       tc_fence_after();
-      const uint32_t kb = smem_u32(sK), vb = smem_u32(sV);
-      for (int n = 0; n < ntiles; ++n) {
-        const int s = n & 1;
-        mbar_wait(&bars[BB_FULL + s], (n >> 1) & 1);
-        tc_fence_after();
-        const uint32_t qb = smem_u32(ring + s * (2 * C::TILE + C::VEC)), ob = qb + C::TILE;
+      const uint32_t qb = smem_u32(ring + s * (2 * C::TILE + C::VEC)), ob = qb + C::TILE;
+      if (elect_one()) {
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) mma_ss(tmem, kmaj<D>(kb, kk), kmaj<D>(qb, kk), IS, kk > 0);
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) mma_ss(tmem + 128, kmaj<D>(vb, kk), kmaj<D>(ob, kk), IS, kk > 0);
         mma_commit(&bars[BB_SFULL]);
-        mbar_wait(&bars[BB_PFULL], n & 1);
-        tc_fence_after();
+      }
+      __syncwarp();
+      mbar_wait(&bars[BB_PFULL], n & 1);
+      tc_fence_after();
+      if (elect_one()) {
 #pragma unroll
         for (int kk = 0; kk < T / 16; ++kk) {
           // Pᵀ / dŜᵀ of queries [64h, 64h + 64) live in columns [64h, 64h + 32) of the Sᵀ / dPᵀ range
@@ -165,8 +169,10 @@ __global__ void __launch_bounds__(kThreadsB, 1)
         }
         mma_commit(&bars[BB_EMPTY + s]);
       }
-      mma_commit(&bars[BB_DONE]);
+      __syncwarp();
     }
+    if (elect_one()) mma_commit(&bars[BB_DONE]);
+    __syncwarp();
   } else if (warp >= 4) {
     const int half = (warp - 4) >> 2, quad = warp & 3;
     const int key = kt * T + quad * 32 + lane;  // this thread's key row (TMEM lane)
@@ -299,32 +305,38 @@ __global__ void __launch_bounds__(kThreadsB, 1)
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t IS = make_idesc_bf16(T, T, false, false);
-      constexpr uint32_t IG = make_idesc_bf16(T, D, false, true);
-      mbar_wait(&bars[BB_KV], 0);
+    // whole warp runs the loop (uniform descriptors), one elected lane issues each batch
+    constexpr uint32_t IS = make_idesc_bf16(T, T, false, false);
+    constexpr uint32_t IG = make_idesc_bf16(T, D, false, true);
+    mbar_wait(&bars[BB_KV], 0);
+    tc_fence_after();
+    const uint32_t qb = smem_u32(sQ), ob = smem_u32(sO);
+    for (int n = 0; n < ntiles; ++n) {
+      const int s = n & 1;
+      mbar_wait(&bars[BB_FULL + s], (n >> 1) & 1);
       tc_fence_after();
-      const uint32_t qb = smem_u32(sQ), ob = smem_u32(sO);
-      for (int n = 0; n < ntiles; ++n) {
-        const int s = n & 1;
-        mbar_wait(&bars[BB_FULL + s], (n >> 1) & 1);
-        tc_fence_after();
-        const uint32_t kb = smem_u32(ring + s * (2 * C::TILE)), vb = kb + C::TILE;
+      const uint32_t kb = smem_u32(ring + s * (2 * C::TILE)), vb = kb + C::TILE;
+      if (elect_one()) {
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) mma_ss(tmem, kmaj<D>(qb, kk), kmaj<D>(kb, kk), IS, kk > 0);
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk) mma_ss(tmem + 128, kmaj<D>(ob, kk), kmaj<D>(vb, kk), IS, kk > 0);
         mma_commit(&bars[BB_SFULL]);
-        mbar_wait(&bars[BB_PFULL], n & 1);
-        tc_fence_after();
+      }
+      __syncwarp();
+      mbar_wait(&bars[BB_PFULL], n & 1);
+      tc_fence_after();
+      if (elect_one()) {
 #pragma unroll
         for (int kk = 0; kk < T / 16; ++kk)
           mma_ts(tmem + 256, tmem + (uint32_t)((kk >> 2) * 64 + (kk & 3) * 8), mnmaj<D>(kb, kk), IG,
                  (n > 0 || kk > 0) ? 1u : 0u);
         mma_commit(&bars[BB_EMPTY + s]);
       }
-      mma_commit(&bars[BB_DONE]);
+      __syncwarp();
     }
+    if (elect_one()) mma_commit(&bars[BB_DONE]);
+    __syncwarp();
   } else if (warp >= 4) {
     const int half = (warp - 4) >> 2, quad = warp & 3;
     const int row = qt * T + quad * 32 + lane;

@@ -2,12 +2,17 @@
 
     python tools/sweep.py [--steps K] > gpurun_out/sweep.json   (one JSON line per case)
 
-Kernel times come from CUDA events recorded around the launches inside the C call
-(distr_attn_set_profile_events); inputs are regenerated per case on the device.
+Call times: CUDA events around 10 back-to-back calls (no per-call events, so the K^T pass and
+the attention kernel may overlap); kernel times from a second pass with events recorded around
+the launches inside the C call (distr_attn_set_profile_events). Each row also carries, on sampled
+Q blocks, the GPU output against the oracle's DistrAttention (parity) and against the exact-
+attention oracle (max-abs, mean-abs, relative Frobenius error: SURVEY §8(c) item 8), and with
+--plan the planner's pick measured. Inputs are regenerated per case on the device.
 """
 import argparse, ctypes, json, os, sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
+import numpy as np
 import torch
 import paper_2507_17245_b200 as da
 from paper_2507_17245_b200 import _native
@@ -18,6 +23,7 @@ ap.add_argument("--steps", type=int, default=10)
 ap.add_argument("--warmup", type=int, default=3)
 ap.add_argument("--only", default="", help="comma-separated case-name prefixes (default: all)")
 ap.add_argument("--block-l", type=int, default=0, help="override block_l of every case (e.g. 256)")
+ap.add_argument("--no-error", action="store_true", help="skip the sampled oracle comparisons")
 ap.add_argument("--plan", action="store_true",
                 help="also run distr_attn_choose's pick for each case (max_group_size = the case's G*)")
 args = ap.parse_args()
@@ -80,6 +86,27 @@ for name, c in cases:
            "distr_tflops_executed": pairs * (2 * DR + 2 * c.d) / (d_attn * 1e-3) / 1e12,
            "exact_tflops": pairs * 4 * c.d / (x_attn * 1e-3) / 1e12,
            "full_d_equiv_tflops": pairs * 4 * c.d / (d_ms * 1e-3) / 1e12}
+    if not args.no_error:
+        # sampled Q blocks (first, last, one random, of two heads): the GPU DistrAttention output
+        # against the oracle's DistrAttention (parity, the north-star tolerance) and against the
+        # exact-attention oracle (the approximation error the config reports)
+        sys.path.insert(0, os.path.join(ROOT, "tests"))
+        from gpu_util import errors, gather_items, oracle_items, valid_rows_mask
+        from synth import sample_items
+        run(None)
+        torch.cuda.synchronize()
+        items = sample_items(c, n_heads=2, per_head=3)
+        got = gather_items(out, items, c.block_l)
+        mask = valid_rows_mask(items, c.N, c.block_l, c.d)
+        want = oracle_items(q, k, v, items, block_l=c.block_l, G=c.group_size, causal=c.causal)
+        ex = oracle_items(q, k, v, items, block_l=c.block_l, G=0, causal=c.causal)
+        pmx, pmean = errors(got, want, mask)
+        emx, emean = errors(got, ex, mask)
+        dg, de = (got - ex)[mask], ex[mask]
+        rec["parity_vs_oracle"] = {"max_abs": pmx, "mean_abs": pmean, "items": len(items),
+                                   "ok": bool(pmx <= 2e-2 and pmean <= 2e-3)}
+        rec["error_vs_exact"] = {"max_abs": emx, "mean_abs": emean,
+                                 "rel_fro": float(np.linalg.norm(dg) / np.linalg.norm(de))}
     if args.plan:
         ch = da.distr_attn_choose(c.B, c.H, c.H_kv, c.N, c.d, causal=c.causal, max_group_size=c.group_size)
         if ch["distr"]:
