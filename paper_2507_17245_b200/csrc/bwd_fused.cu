@@ -33,7 +33,8 @@ namespace {
 constexpr int T = 128;            // rows per tile (queries or keys)
 constexpr int kThreadsB = 384;    // warp 0 TMA, warp 1 MMA, warps 4..11 elementwise
 
-enum { BB_KV = 0, BB_FULL = 1, BB_EMPTY = 3, BB_SFULL = 5, BB_PFULL = 6, BB_DONE = 7, BB_TMEM = 8, BB_N = 9 };
+// SFULL / PFULL per 64-row half h of the tile pair's score block (+h)
+enum { BB_KV = 0, BB_FULL = 1, BB_EMPTY = 3, BB_SFULL = 5, BB_PFULL = 7, BB_DONE = 9, BB_TMEM = 10, BB_N = 11 };
 
 template <int D>
 struct BCfg {
@@ -105,8 +106,10 @@ __global__ void __launch_bounds__(kThreadsB, 1)
       mbar_init(&bars[BB_FULL + s], 1);
       mbar_init(&bars[BB_EMPTY + s], 1);
     }
-    mbar_init(&bars[BB_SFULL], 1);
-    mbar_init(&bars[BB_PFULL], 256);
+    for (int hh = 0; hh < 2; ++hh) {
+      mbar_init(&bars[BB_SFULL + hh], 1);
+      mbar_init(&bars[BB_PFULL + hh], 128);  // the 4 elementwise warps of half hh
+    }
     mbar_init(&bars[BB_DONE], 1);
     fence_mbar_init();
   }
@@ -139,37 +142,58 @@ __global__ void __launch_bounds__(kThreadsB, 1)
     }
   } else if (warp == 1) {
     // whole warp runs the loop (uniform descriptors), one elected lane issues each batch
-    constexpr uint32_t IS = make_idesc_bf16(T, T, false, false);   // Sᵀ, dPᵀ
-    constexpr uint32_t IG = make_idesc_bf16(T, D, false, true);    // dV, dK (B MN-major)
+    // Half-split pipeline: the score block of a tile is computed and consumed in two halves of 64
+    // queries (N = 64): while the elementwise warps of one half work, the tensor core runs the
+    // other half's dV/dK and the next tile's Sᵀ/dPᵀ half; Sᵀ_h(n+1) overwrites Pᵀ_h(n) in TMEM,
+    // so it follows dV/dK_h(n) in the in-order pipe.
+    constexpr uint32_t IS = make_idesc_bf16(T, T / 2, false, false);  // Sᵀ, dPᵀ halves
+    constexpr uint32_t IG = make_idesc_bf16(T, D, false, true);       // dV, dK (B MN-major)
     mbar_wait(&bars[BB_KV], 0);
     tc_fence_after();
     const uint32_t kb = smem_u32(sK), vb = smem_u32(sV);
+    constexpr uint32_t HROW = (T / 2) * Box<D>::ROW;  // byte offset of row 64 inside a box
+    auto issue_s = [&](int n, int hh) {  // Sᵀ / dPᵀ of queries [64hh, 64hh + 64) of tile n
+      const int s = n & 1;
+      if (hh == 0) mbar_wait(&bars[BB_FULL + s], (n >> 1) & 1);
+      tc_fence_after();
+      const uint32_t qb = smem_u32(ring + s * (2 * C::TILE + C::VEC)) + hh * HROW, ob = qb + C::TILE;
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          mma_ss(tmem + 64 * hh, kmaj<D>(kb, kk), kmaj<D>(qb, kk), IS, kk > 0);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          mma_ss(tmem + 128 + 64 * hh, kmaj<D>(vb, kk), kmaj<D>(ob, kk), IS, kk > 0);
+        mma_commit(&bars[BB_SFULL + hh]);
+      }
+      __syncwarp();
+    };
+    if (ntiles > 0) {
+      issue_s(0, 0);
+      issue_s(0, 1);
+    }
     for (int n = 0; n < ntiles; ++n) {
       const int s = n & 1;
-      mbar_wait(&bars[BB_FULL + s], (n >> 1) & 1);
-      tc_fence_after();
       const uint32_t qb = smem_u32(ring + s * (2 * C::TILE + C::VEC)), ob = qb + C::TILE;
-      if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) mma_ss(tmem, kmaj<D>(kb, kk), kmaj<D>(qb, kk), IS, kk > 0);
+      for (int hh = 0; hh < 2; ++hh) {
+        mbar_wait(&bars[BB_PFULL + hh], n & 1);
+        tc_fence_after();
+        if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) mma_ss(tmem + 128, kmaj<D>(vb, kk), kmaj<D>(ob, kk), IS, kk > 0);
-        mma_commit(&bars[BB_SFULL]);
-      }
-      __syncwarp();
-      mbar_wait(&bars[BB_PFULL], n & 1);
-      tc_fence_after();
-      if (elect_one()) {
-#pragma unroll
-        for (int kk = 0; kk < T / 16; ++kk) {
-          // Pᵀ / dŜᵀ of queries [64h, 64h + 64) live in columns [64h, 64h + 32) of the Sᵀ / dPᵀ range
-          const uint32_t pc = (uint32_t)((kk >> 2) * 64 + (kk & 3) * 8);
-          mma_ts(tmem + 256, tmem + pc, mnmaj<D>(ob, kk), IG, (n > 0 || kk > 0) ? 1u : 0u);
-          mma_ts(tmem + 384, tmem + 128 + pc, mnmaj<D>(qb, kk), IG, (n > 0 || kk > 0) ? 1u : 0u);
+          for (int k4 = 0; k4 < 4; ++k4) {
+            // Pᵀ / dŜᵀ of queries [64hh, 64hh + 64) live in columns [64hh, 64hh + 32)
+            const int kk = 4 * hh + k4;
+            const uint32_t pc = (uint32_t)(64 * hh + 8 * k4);
+            const uint32_t acc = (n > 0 || kk > 0) ? 1u : 0u;
+            mma_ts(tmem + 256, tmem + pc, mnmaj<D>(ob, kk), IG, acc);
+            mma_ts(tmem + 384, tmem + 128 + pc, mnmaj<D>(qb, kk), IG, acc);
+          }
+          if (hh == 1) mma_commit(&bars[BB_EMPTY + s]);
         }
-        mma_commit(&bars[BB_EMPTY + s]);
+        __syncwarp();
+        if (n + 1 < ntiles) issue_s(n + 1, hh);
       }
-      __syncwarp();
     }
     if (elect_one()) mma_commit(&bars[BB_DONE]);
     __syncwarp();
@@ -182,7 +206,7 @@ __global__ void __launch_bounds__(kThreadsB, 1)
       const int s = n & 1;
       int bh, qt;
       tile_of(n, &bh, &qt);
-      mbar_wait(&bars[BB_SFULL], n & 1);
+      mbar_wait(&bars[BB_SFULL + half], n & 1);
       tc_fence_after();
       const float* vec = reinterpret_cast<const float*>(ring + s * (2 * C::TILE + C::VEC) + 2 * C::TILE);
       // two 32-query chunks of this half: Sᵀ, dPᵀ chunk -> Pᵀ, dŜᵀ (bf16) into the first halves of
@@ -217,7 +241,7 @@ __global__ void __launch_bounds__(kThreadsB, 1)
       }
       tmem_st_wait();
       tc_fence_before();
-      mbar_arrive(&bars[BB_PFULL]);
+      mbar_arrive(&bars[BB_PFULL + half]);
     }
     // epilogue: dV, dK rows of this key (each half writes d/2 columns)
     mbar_wait(&bars[BB_DONE], 0);
@@ -276,8 +300,10 @@ __global__ void __launch_bounds__(kThreadsB, 1)
       mbar_init(&bars[BB_FULL + s], 1);
       mbar_init(&bars[BB_EMPTY + s], 1);
     }
-    mbar_init(&bars[BB_SFULL], 1);
-    mbar_init(&bars[BB_PFULL], 256);
+    for (int hh = 0; hh < 2; ++hh) {
+      mbar_init(&bars[BB_SFULL + hh], 1);
+      mbar_init(&bars[BB_PFULL + hh], 128);  // the 4 elementwise warps of half hh
+    }
     mbar_init(&bars[BB_DONE], 1);
     fence_mbar_init();
   }
@@ -306,34 +332,52 @@ __global__ void __launch_bounds__(kThreadsB, 1)
     }
   } else if (warp == 1) {
     // whole warp runs the loop (uniform descriptors), one elected lane issues each batch
-    constexpr uint32_t IS = make_idesc_bf16(T, T, false, false);
+    // Half-split pipeline over the 64-key halves of each K/V tile (see the dK/dV kernel).
+    constexpr uint32_t IS = make_idesc_bf16(T, T / 2, false, false);
     constexpr uint32_t IG = make_idesc_bf16(T, D, false, true);
     mbar_wait(&bars[BB_KV], 0);
     tc_fence_after();
     const uint32_t qb = smem_u32(sQ), ob = smem_u32(sO);
+    constexpr uint32_t HROW = (T / 2) * Box<D>::ROW;
+    auto issue_s = [&](int n, int hh) {  // S / dP of keys [64hh, 64hh + 64) of K/V tile n
+      const int s = n & 1;
+      if (hh == 0) mbar_wait(&bars[BB_FULL + s], (n >> 1) & 1);
+      tc_fence_after();
+      const uint32_t kb = smem_u32(ring + s * (2 * C::TILE)) + hh * HROW, vb = kb + C::TILE;
+      if (elect_one()) {
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          mma_ss(tmem + 64 * hh, kmaj<D>(qb, kk), kmaj<D>(kb, kk), IS, kk > 0);
+#pragma unroll
+        for (int kk = 0; kk < D / 16; ++kk)
+          mma_ss(tmem + 128 + 64 * hh, kmaj<D>(ob, kk), kmaj<D>(vb, kk), IS, kk > 0);
+        mma_commit(&bars[BB_SFULL + hh]);
+      }
+      __syncwarp();
+    };
+    if (ntiles > 0) {
+      issue_s(0, 0);
+      issue_s(0, 1);
+    }
     for (int n = 0; n < ntiles; ++n) {
       const int s = n & 1;
-      mbar_wait(&bars[BB_FULL + s], (n >> 1) & 1);
-      tc_fence_after();
-      const uint32_t kb = smem_u32(ring + s * (2 * C::TILE)), vb = kb + C::TILE;
-      if (elect_one()) {
+      const uint32_t kb = smem_u32(ring + s * (2 * C::TILE));
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) mma_ss(tmem, kmaj<D>(qb, kk), kmaj<D>(kb, kk), IS, kk > 0);
+      for (int hh = 0; hh < 2; ++hh) {
+        mbar_wait(&bars[BB_PFULL + hh], n & 1);
+        tc_fence_after();
+        if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk) mma_ss(tmem + 128, kmaj<D>(ob, kk), kmaj<D>(vb, kk), IS, kk > 0);
-        mma_commit(&bars[BB_SFULL]);
+          for (int k4 = 0; k4 < 4; ++k4) {
+            const int kk = 4 * hh + k4;
+            mma_ts(tmem + 256, tmem + (uint32_t)(64 * hh + 8 * k4), mnmaj<D>(kb, kk), IG,
+                   (n > 0 || kk > 0) ? 1u : 0u);
+          }
+          if (hh == 1) mma_commit(&bars[BB_EMPTY + s]);
+        }
+        __syncwarp();
+        if (n + 1 < ntiles) issue_s(n + 1, hh);
       }
-      __syncwarp();
-      mbar_wait(&bars[BB_PFULL], n & 1);
-      tc_fence_after();
-      if (elect_one()) {
-#pragma unroll
-        for (int kk = 0; kk < T / 16; ++kk)
-          mma_ts(tmem + 256, tmem + (uint32_t)((kk >> 2) * 64 + (kk & 3) * 8), mnmaj<D>(kb, kk), IG,
-                 (n > 0 || kk > 0) ? 1u : 0u);
-        mma_commit(&bars[BB_EMPTY + s]);
-      }
-      __syncwarp();
     }
     if (elect_one()) mma_commit(&bars[BB_DONE]);
     __syncwarp();
@@ -345,7 +389,7 @@ __global__ void __launch_bounds__(kThreadsB, 1)
     const float lse2 = a.lse_pad[(size_t)bh * a.N_pad + row] * 1.4426950408889634f;
     const float dd = a.D_pad[(size_t)bh * a.N_pad + row];
     for (int n = 0; n < ntiles; ++n) {
-      mbar_wait(&bars[BB_SFULL], n & 1);
+      mbar_wait(&bars[BB_SFULL + half], n & 1);
       tc_fence_after();
 #pragma unroll
       for (int c2 = 0; c2 < 2; ++c2) {
@@ -371,7 +415,7 @@ __global__ void __launch_bounds__(kThreadsB, 1)
       }
       tmem_st_wait();
       tc_fence_before();
-      mbar_arrive(&bars[BB_PFULL]);
+      mbar_arrive(&bars[BB_PFULL + half]);
     }
     mbar_wait(&bars[BB_DONE], 0);
     tc_fence_after();
