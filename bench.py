@@ -318,6 +318,21 @@ def main():
     achieved = exec_f / (attn_ms * 1e-3) / 1e12
     traffic, traffic_src = load_traffic(args.config)
 
+    exps = (heads[1] - heads[0]) * cfg.N * cfg.N * (0.5 if cfg.causal else 1.0)
+    if args.shard == "q":
+        exps /= world
+
+    def mufu_line(n_exp, kms, clk, mufu_share):
+        mhz = clk.get("sm_mhz")
+        if not mhz:
+            return None
+        peak_exp = 16 * SM_COUNT * mhz * 1e6  # MUFU.EX2 per second
+        rate = n_exp / (kms * 1e-3)
+        return {"bound": "mufu", "exp2_per_s": rate, "mufu_ops_per_s": rate * mufu_share,
+                "peak_mufu_ops_per_s": peak_exp, "frac": rate * mufu_share / peak_exp,
+                "note": "MUFU.EX2 ops (the pairs not on the FMA-pipe polynomial) / (16 per clk per SM x "
+                        "148 SMs x the sampled SM clock)"}
+
     def pipe_frac(flop, kms, clk):  # tensor-pipe share at the SM clock measured during the run
         mhz = clk.get("sm_mhz")
         return None if not mhz else flop / (kms * 1e-3) / (TC_FLOP_PER_CLK_SM * SM_COUNT * mhz * 1e6)
@@ -436,6 +451,10 @@ def main():
                          "tensor_pipe_frac_at_clock_note":
                              f"executed FLOP/s / ({TC_FLOP_PER_CLK_SM} FLOP/clk/SM x {SM_COUNT} SMs x "
                              "the median SM clock sampled during the timed region)"},
+            # the resource that binds both kernels on B200: one exp2 per (query, key)
+            # pair; MUFU.EX2 16/clk/SM (measured, tools/mb) at the SM clock sampled during the run;
+            # EMU/8 of the pairs run on the FMA pipe instead (the distr default EMU = 2)
+            "mufu_roofline": mufu_line(exps, attn_ms, clocks, 0.75),
             "exact_roofline_frac": exec_f_ex / (ex_attn_ms * 1e-3) / 1e12 / peak,
             "exact_tensor_pipe_frac_at_clock": pipe_frac(exec_f_ex, ex_attn_ms, ex_clocks),
             "planner": da.distr_attn_choose(cfg.B, cfg.H, cfg.H_kv, cfg.N, cfg.d, causal=cfg.causal,
