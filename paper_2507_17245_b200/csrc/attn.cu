@@ -34,10 +34,6 @@
 #include "internal.h"
 #include "ptx.cuh"
 
-#ifndef DA_HASH_UNROLL
-#define DA_HASH_UNROLL 8
-#endif
-constexpr int kHashUnroll = DA_HASH_UNROLL;  // rows of the projection chain unrolled
 #ifndef DA_SPLIT
 #define DA_SPLIT 2
 #endif
@@ -218,10 +214,18 @@ DA_DEV void qhat_prologue(const AttnArgs& args, uint64_t* bars, const uint8_t* s
 #pragma unroll
       for (int m = 0; m < KG / 2; ++m) ya[m] = yb[m] = make_float2(0.0f, 0.0f);
       const float* pr = proj_t + KG * kg;
-#pragma unroll kHashUnroll
-      for (int r = 0; r < rows; ++r) {  // ascending rows: the R6 fp32 fma chain
-        const uint32_t q2 = *reinterpret_cast<const uint32_t*>(
-            sQ + (C::SHARED ? q_off(r >> 7, r & (BM - 1), c) : q_off(t, hb * L + r, c)));
+      // staged-Q address of row rr (of the hash block) for this thread's column pair: the swizzle
+      // XOR term depends only on rr % 8, so the 8 per-row column offsets are precomputed and the
+      // row loop runs in blocks of 8 (one add per row instead of the full swizzle arithmetic)
+      constexpr uint32_t ROWB = C::RB * 2;
+      uint32_t xo[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) xo[j] = swz(j * ROWB + (uint32_t)(c % C::RB) * 2, C::RB_SWB) - j * ROWB;
+      const uint32_t cbase = (uint32_t)((c / C::RB) * (BM * C::RB * 2));
+      auto hash_row = [&](int r, uint32_t x) {  // ascending rows: the R6 fp32 fma chain
+        const uint32_t addr = C::SHARED ? (uint32_t)((r >> 7) * C::QT_BYTES) + cbase + (r & (BM - 1)) * ROWB + x
+                                        : (uint32_t)(t * C::QT_BYTES) + cbase + (hb * L + r) * ROWB + x;
+        const uint32_t q2 = *reinterpret_cast<const uint32_t*>(sQ + addr);
         const float qa = __uint_as_float(q2 << 16), qb = __uint_as_float(q2 & 0xFFFF0000u);
         float2 pk[KG / 2];
         if constexpr (KG == 2) {
@@ -239,7 +243,14 @@ DA_DEV void qhat_prologue(const AttnArgs& args, uint64_t* bars, const uint8_t* s
           ya[m] = fma2(pk[m], make_float2(qa, qa), ya[m]);
           yb[m] = fma2(pk[m], make_float2(qb, qb), yb[m]);
         }
+      };
+      int r = 0;
+      for (; r + 8 <= rows; r += 8) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) hash_row(r + j, xo[j]);
       }
+      for (; r < rows; ++r)  // ragged tail of the block (rare): the swizzle term recomputed
+        hash_row(r, swz((r & 7) * ROWB + (uint32_t)(c % C::RB) * 2, C::RB_SWB) - (r & 7) * ROWB);
       uint32_t ba = 0, bb = 0;
 #pragma unroll
       for (int m = 0; m < KG / 2; ++m) {
