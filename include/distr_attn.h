@@ -202,7 +202,7 @@ int distr_attn_plan(int N, int d, int block_l, int group_size, int distr, da_pla
  * accuracy bound: G* = 1 is exact attention, error grows with G*, Tables 3-4), and returns the
  * fastest. Model per CTA (two 128-row Q tiles): prologue clk + key-tile steps x step clk (CTA
  * timelines, tools/calibrate.sh), CTAs list-scheduled over 148 SMs at clk_mhz (<= 0: 1800), plus
- * the K^T pass (HBM-bound) and launch overhead; DistrAttention is chosen only when predicted >= 3 %
+ * the K^T pass (HBM-bound) and launch overhead; DistrAttention is chosen only when predicted >= 2 %
  * faster than the exact kernel (the model's spread; exact attention is the more accurate). Host-only. Returns DA_OK, DA_ERR_INVALID (NULL
  * out, non-positive dims, H % H_kv) or DA_ERR_PRECONDITION (d not in {32, 64, 128}). */
 typedef struct da_choice {

@@ -903,8 +903,8 @@ int distr_attn_choose(int B, int H, int H_kv, int N, int d, int causal, int max_
     }
   }
   // the approximation is taken only when it is predicted clearly faster than exact attention
-  // (more accurate by definition): by more than the model's spread against the sweeps, 3 %
-  out->distr = out->predicted_distr_us < 0.97 * out->predicted_exact_us;
+  // (more accurate by definition): by more than the model's spread against the sweeps, 2 %
+  out->distr = out->predicted_distr_us < 0.98 * out->predicted_exact_us;
   out->predicted_us = out->distr ? out->predicted_distr_us : out->predicted_exact_us;
   if (!out->distr) {
     out->block_l = 0;
