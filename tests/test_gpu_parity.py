@@ -317,3 +317,15 @@ def test_cuda_graph_capture_and_replay():
         g.replay()
     torch.cuda.synchronize()
     assert torch.equal(out, ref) and torch.equal(ex, ex_ref)
+
+
+def test_host_entry_point_fp32_chunked(monkeypatch):
+    # fp32 inputs through the chunked host path (4-byte elements, prep hash + conversions per chunk)
+    monkeypatch.setenv("DA_HOST_CHUNK_UNITS", "1")
+    cfg = cfg_small(B=1, H=3, H_kv=3, N=300, d=64, block_l=64, dtype="f32")
+    q, k, v = make_qkv(cfg, device=DEV)
+    out = da.distr_attn_fwd_ex(q, k, v, block_l=64, group_size=2, seed=2)
+    torch.cuda.synchronize()
+    oh = da.distr_attn_fwd_host(q.cpu().pin_memory(), k.cpu().pin_memory(), v.cpu().pin_memory(),
+                                block_l=64, group_size=2, seed=2)
+    assert torch.equal(oh, out.cpu())
