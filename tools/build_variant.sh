@@ -10,5 +10,5 @@ for f in api prep prep_global bwd bwd_fused attn; do
     --expt-relaxed-constexpr -I$R/include "$@" -c $R/paper_2507_17245_b200/csrc/$f.cu -o $O/$f.o -Xptxas -v 2> $O/$f.log &
 done
 wait
-/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $R/tools/exp/lib_$name.so $O/api.o $O/prep.o $O/prep_global.o $O/bwd.o $O/bwd_fused.o $O/attn.o -lcublas
+/usr/local/cuda/bin/nvcc -gencode arch=compute_100a,code=sm_100a -shared -o $R/tools/exp/lib_$name.so $O/api.o $O/prep.o $O/prep_global.o $O/bwd.o $O/bwd_fused.o $O/attn.o
 echo $R/tools/exp/lib_$name.so
