@@ -32,6 +32,12 @@ namespace {
 
 constexpr int T = 128;            // rows per tile (queries or keys)
 constexpr int kThreadsB = 384;    // warp 0 TMA, warp 1 MMA, warps 4..11 elementwise
+// exp2 pairs (of every 8) evaluated by the FMA-pipe polynomial instead of MUFU.EX2 (as the forward's
+// EMU); overridable at build time for A/B runs
+#ifndef DA_BWD_EMU
+#define DA_BWD_EMU 2
+#endif
+constexpr int kBwdEmu = DA_BWD_EMU;
 
 // SFULL / PFULL per 64-row half h of the tile pair's score block (+h)
 enum { BB_KV = 0, BB_FULL = 1, BB_EMPTY = 3, BB_SFULL = 5, BB_PFULL = 7, BB_DONE = 9, BB_TMEM = 10, BB_N = 11 };
@@ -202,6 +208,8 @@ __global__ void __launch_bounds__(kThreadsB, 1)
     const int key = kt * T + quad * 32 + lane;  // this thread's key row (TMEM lane)
     const uint32_t lb = (uint32_t)(quad * 32) << 16;
     const float sl2 = a.scale * 1.4426950408889634f, l2e = 1.4426950408889634f;
+    const float2 sl2x2 = make_float2(sl2, sl2), nl2e2 = make_float2(-l2e, -l2e), zero2 = make_float2(0.f, 0.f),
+                 sc2 = make_float2(a.scale, a.scale);
     for (int n = 0; n < ntiles; ++n) {
       const int s = n & 1;
       int bh, qt;
@@ -223,17 +231,22 @@ __global__ void __launch_bounds__(kThreadsB, 1)
         uint32_t pk[16], dk2[16];
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
-          float p2[2], d2[2];
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const int c = 2 * e + u;
-            float p = ex2(__uint_as_float(sr[c]) * sl2 - lv[c] * l2e);
-            if (a.causal && key > q0 + c) p = 0.f;
-            p2[u] = p;
-            d2[u] = p * (__uint_as_float(pr[c]) - dv[c]) * a.scale;
+          // x = S·scale·log2e − lse·log2e (FFMA2), exp2 on MUFU or, for kBwdEmu of every 8 pairs,
+          // the FMA-pipe polynomial (the elementwise phase is MUFU-bound at d <= 64)
+          const float2 l2 = *reinterpret_cast<const float2*>(lv + 2 * e);
+          const float2 x = fma2(make_float2(__uint_as_float(sr[2 * e]), __uint_as_float(sr[2 * e + 1])), sl2x2,
+                                fma2(l2, nl2e2, zero2));
+          float2 p = (e & 7) >= 8 - kBwdEmu ? exp2_poly2(x) : make_float2(ex2(x.x), ex2(x.y));
+          if (a.causal) {
+            if (key > q0 + 2 * e) p.x = 0.f;
+            if (key > q0 + 2 * e + 1) p.y = 0.f;
           }
-          pk[e] = pack_bf16x2(p2[0], p2[1]);
-          dk2[e] = pack_bf16x2(d2[0], d2[1]);
+          const float2 d2 = *reinterpret_cast<const float2*>(dv + 2 * e);
+          const float2 g = fadd2(make_float2(__uint_as_float(pr[2 * e]), __uint_as_float(pr[2 * e + 1])),
+                                 make_float2(-d2.x, -d2.y));
+          const float2 ds = fma2(fma2(p, g, zero2), sc2, zero2);
+          pk[e] = pack_bf16x2(p.x, p.y);
+          dk2[e] = pack_bf16x2(ds.x, ds.y);
         }
         // into this half's own columns (no other warp reads them): no race with the other half
         tmem_st16(tmem + lb + 64 * half + 16 * c2, pk);
@@ -388,6 +401,8 @@ __global__ void __launch_bounds__(kThreadsB, 1)
     const float sl2 = a.scale * 1.4426950408889634f;
     const float lse2 = a.lse_pad[(size_t)bh * a.N_pad + row] * 1.4426950408889634f;
     const float dd = a.D_pad[(size_t)bh * a.N_pad + row];
+    const float2 sl2x2 = make_float2(sl2, sl2), nlse2 = make_float2(-lse2, -lse2), nd2 = make_float2(-dd, -dd),
+                 zero2 = make_float2(0.f, 0.f), sc2 = make_float2(a.scale, a.scale);
     for (int n = 0; n < ntiles; ++n) {
       mbar_wait(&bars[BB_SFULL + half], n & 1);
       tc_fence_after();
@@ -401,15 +416,15 @@ __global__ void __launch_bounds__(kThreadsB, 1)
         uint32_t dk2[16];
 #pragma unroll
         for (int e = 0; e < 16; ++e) {
-          float d2[2];
-#pragma unroll
-          for (int u = 0; u < 2; ++u) {
-            const int c = 2 * e + u;
-            float p = ex2(__uint_as_float(sr[c]) * sl2 - lse2);
-            if (a.causal && k0 + c > row) p = 0.f;
-            d2[u] = p * (__uint_as_float(pr[c]) - dd) * a.scale;
+          const float2 x = fma2(make_float2(__uint_as_float(sr[2 * e]), __uint_as_float(sr[2 * e + 1])), sl2x2, nlse2);
+          float2 p = (e & 7) >= 8 - kBwdEmu ? exp2_poly2(x) : make_float2(ex2(x.x), ex2(x.y));
+          if (a.causal) {
+            if (k0 + 2 * e > row) p.x = 0.f;
+            if (k0 + 2 * e + 1 > row) p.y = 0.f;
           }
-          dk2[e] = pack_bf16x2(d2[0], d2[1]);
+          const float2 g = fadd2(make_float2(__uint_as_float(pr[2 * e]), __uint_as_float(pr[2 * e + 1])), nd2);
+          const float2 ds = fma2(fma2(p, g, zero2), sc2, zero2);
+          dk2[e] = pack_bf16x2(ds.x, ds.y);
         }
         tmem_st16(tmem + lb + 64 * half + 16 * c2, dk2);
       }
