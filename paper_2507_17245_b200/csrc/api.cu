@@ -499,7 +499,7 @@ int bwd_workspace(const da_params* p, size_t need, int* dev, cudaStream_t st, Sc
 }
 
 // Fused tcgen05 backward (bwd_fused.cu): hash -> Q̃ + D + padded lse -> dK/dV kernel -> dQ̃ kernel
-// -> fold. d in {32, 64, 128}.
+// (dQ̃ folded onto the representatives in its epilogue). d in {32, 64, 128}.
 int backward_fused(const void* q, const void* k, const void* v, const void* o, const void* dout, const float* lse,
                    void* dq, void* dk, void* dv, const da_params* p, const Plan& P, cudaStream_t st) {
   int dev = 0;
@@ -508,7 +508,7 @@ int backward_fused(const void* q, const void* k, const void* v, const void* o, c
   size_t o_ = 0;
   auto take = [&](size_t bytes) { size_t at = o_; o_ = al256(o_ + bytes); return at; };
   const size_t off_perm = take(BH * P.nqb * d), off_qt = take(BH * N * d * 2), off_D = take(BH * N_pad * 4);
-  const size_t off_lse = take(BH * N_pad * 4), off_dqt = take(BH * N * d * 4);
+  const size_t off_lse = take(BH * N_pad * 4);
   Scratch sc;
   uint8_t* ws;
   if (int s = bwd_workspace(p, o_, &dev, st, sc, &ws)) return s;
@@ -539,17 +539,17 @@ int backward_fused(const void* q, const void* k, const void* v, const void* o, c
   da::BwdFusedArgs f{};
   f.tmQt = &tmQt; f.tmdO = &tmdO; f.tmK = &tmK; f.tmV = &tmV;
   f.lse_pad = lse_pad; f.D_pad = a.D;
-  f.dqt = reinterpret_cast<float*>(ws + off_dqt);
+  f.dq = static_cast<uint16_t*>(dq);
+  f.perm = a.perm; f.G = P.G; f.nqb = P.nqb; f.block_l = P.l;
   f.dk = static_cast<uint16_t*>(dk); f.dv = static_cast<uint16_t*>(dv);
   f.BH = (int)BH; f.BHkv = (int)BHkv; f.H = P.H; f.Hkv = P.Hkv; f.N = P.N; f.N_pad = (int)N_pad; f.d = P.d;
   f.causal = P.causal; f.scale = P.scale;
   record_ev(0, st);
   DA_CUDA(da::launch_bwd_fused(f, st));
   record_ev(1, st);
-  DA_CUDA(da::launch_fold_all(f.dqt, a.perm, static_cast<uint16_t*>(dq), (int)BH, P.N, P.d, P.G, P.nqb, P.l, st));
   record_ev(2, st);
   g_ev[0] = g_ev[1] = g_ev[2] = nullptr;
-  g_last_launches = 6;  // hash, Q̃/D, lse pad, dK/dV, dQ̃, fold
+  g_last_launches = 5;  // hash, Q̃/D, lse pad, dK/dV, dQ̃ (+ fold in its epilogue)
   return DA_OK;
 }
 

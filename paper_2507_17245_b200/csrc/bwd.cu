@@ -7,7 +7,7 @@
 //   folds onto the representatives: dQ[r][rep_j] = Σ_{c ∈ G_j} dQ̃[r][c] (zero elsewhere).
 //
 // Kernels: qtilde (Q̃ rows + D[r] = Σ dO∘O), lse_pad (the forward's LSE padded with +inf to whole
-// 128-row tiles), fold_all (dQ from the fp32 dQ̃ workspace).
+// 128-row tiles). The fold dQ̃ -> dQ runs in the dQ̃ kernel's epilogue (bwd_fused.cu).
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -21,33 +21,49 @@ namespace {
 __device__ __forceinline__ float bf2f(uint16_t x) { return __uint_as_float(((uint32_t)x) << 16); }
 __device__ __forceinline__ uint16_t f2bf(float x) { return __bfloat16_as_ushort(__float2bfloat16_rn(x)); }
 
-// One CTA per (bh, 64-row slab inside one Q block). rep map from the block's permutation.
-__global__ void qtilde_kernel(const BwdArgs a) {
-  __shared__ uint8_t rep_s[256];
-  __shared__ uint8_t inv_s[256];
+// One CTA per (bh, 64-row slab inside one Q block; block_l >= 64). The slab's Q rows are staged in
+// shared memory with 16-byte loads; each thread then writes 16-byte chunks of Q̃ (8 gathered
+// representatives) and the dot products D[r] = Σ dO∘O are reduced over the CPR lanes of a row.
+template <int D>
+__global__ void __launch_bounds__(256) qtilde_kernel(const BwdArgs a) {
+  constexpr int CPR = D / 8, QP = D + 8;  // 16-byte chunks per row, staging pitch (elements)
+  __shared__ __align__(16) uint16_t q_s[64 * QP];
+  __shared__ uint8_t rep_s[D], inv_s[D];
   const int bh = blockIdx.y;
   const int r0 = blockIdx.x * 64;
   const int qb = r0 / a.block_l;
-  const uint8_t* perm = a.perm + ((size_t)bh * a.nqb + qb) * a.d;
-  for (int i = threadIdx.x; i < a.d; i += blockDim.x) inv_s[perm[i]] = (uint8_t)i;
-  __syncthreads();
-  for (int c = threadIdx.x; c < a.d; c += blockDim.x) rep_s[c] = perm[(inv_s[c] / a.G) * a.G];
-  __syncthreads();
+  const uint8_t* perm = a.perm + ((size_t)bh * a.nqb + qb) * D;
+  for (int i = threadIdx.x; i < D; i += blockDim.x) inv_s[perm[i]] = (uint8_t)i;
   const int rows = min(64, a.N - r0);
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
-  for (int r = warp; r < rows; r += blockDim.x / 32) {
-    const size_t row = (size_t)bh * a.N + r0 + r;
-    const uint16_t* q = a.q + row * a.d;
-    const uint16_t* o = a.o + row * a.d;
-    const uint16_t* g = a.dout + row * a.d;
+  const size_t base = ((size_t)bh * a.N + r0) * D;
+  for (int i = threadIdx.x; i < 64 * CPR; i += blockDim.x) {
+    const int r = i / CPR, ch = i % CPR;
     float acc = 0.f;
-    for (int c = lane; c < a.d; c += 32) {
-      a.qt[row * a.d + c] = q[rep_s[c]];
-      acc += bf2f(g[c]) * bf2f(o[c]);
+    if (r < rows) {
+      const uint4 qv = *reinterpret_cast<const uint4*>(a.q + base + (size_t)r * D + 8 * ch);
+      *reinterpret_cast<uint4*>(q_s + r * QP + 8 * ch) = qv;
+      const uint4 ov = *reinterpret_cast<const uint4*>(a.o + base + (size_t)r * D + 8 * ch);
+      const uint4 gv = *reinterpret_cast<const uint4*>(a.dout + base + (size_t)r * D + 8 * ch);
+      const uint32_t ow[4] = {ov.x, ov.y, ov.z, ov.w}, gw[4] = {gv.x, gv.y, gv.z, gv.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e)
+        acc += bf2f((uint16_t)(gw[e] & 0xFFFF)) * bf2f((uint16_t)(ow[e] & 0xFFFF)) +
+               bf2f((uint16_t)(gw[e] >> 16)) * bf2f((uint16_t)(ow[e] >> 16));
     }
 #pragma unroll
-    for (int s = 16; s > 0; s >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, s);
-    if (lane == 0) a.D[(size_t)bh * a.Dstride + r0 + r] = acc;
+    for (int m = 1; m < CPR; m <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
+    if (ch == 0 && r < rows) a.D[(size_t)bh * a.Dstride + r0 + r] = acc;
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < D; c += blockDim.x) rep_s[c] = perm[(inv_s[c] / a.G) * a.G];
+  __syncthreads();
+  for (int i = threadIdx.x; i < rows * CPR; i += blockDim.x) {
+    const int r = i / CPR, ch = i % CPR;
+    uint32_t w[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      w[e] = (uint32_t)q_s[r * QP + rep_s[8 * ch + 2 * e]] | ((uint32_t)q_s[r * QP + rep_s[8 * ch + 2 * e + 1]] << 16);
+    *reinterpret_cast<uint4*>(a.qt + base + (size_t)r * D + 8 * ch) = make_uint4(w[0], w[1], w[2], w[3]);
   }
 }
 
@@ -61,35 +77,16 @@ __global__ void lse_pad_kernel(const float* lse, float* out, int BH, int N, int 
   }
 }
 
-// dQ[r][rep_j] = Σ_{c in G_j} dQ̃[r][c] over whole rows (fused path); non-representatives 0.
-__global__ void fold_all_kernel(const float* dqt, const uint8_t* perm, uint16_t* dq, int N, int d, int G, int nqb,
-                                int block_l) {
-  const int r = blockIdx.x, bh = blockIdx.y;
-  const uint8_t* pm = perm + ((size_t)bh * nqb + r / block_l) * d;
-  const float* src = dqt + ((size_t)bh * N + r) * d;
-  uint16_t* dst = dq + ((size_t)bh * N + r) * d;
-  for (int i = threadIdx.x; i < d; i += blockDim.x) dst[i] = 0;
-  __syncthreads();
-  for (int j = threadIdx.x; j < d / G; j += blockDim.x) {
-    float s = 0.f;
-    for (int g = 0; g < G; ++g) s += src[pm[j * G + g]];
-    dst[pm[j * G]] = f2bf(s);
-  }
-}
-
 }  // namespace
 
 cudaError_t launch_bwd_prologue(const BwdArgs& a, const float* lse, float* lse_pad, int N_pad, cudaStream_t st) {
   cudaError_t e = cudaMemsetAsync(a.D, 0, (size_t)a.BH * N_pad * 4, st);
   if (e != cudaSuccess) return e;
-  qtilde_kernel<<<dim3((a.N + 63) / 64, a.BH), 256, 0, st>>>(a);
+  const dim3 grid((a.N + 63) / 64, a.BH);
+  if (a.d == 32) qtilde_kernel<32><<<grid, 256, 0, st>>>(a);
+  else if (a.d == 64) qtilde_kernel<64><<<grid, 256, 0, st>>>(a);
+  else qtilde_kernel<128><<<grid, 256, 0, st>>>(a);
   lse_pad_kernel<<<grid_for((size_t)a.BH * N_pad), 256, 0, st>>>(lse, lse_pad, a.BH, a.N, N_pad);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_fold_all(const float* dqt, const uint8_t* perm, uint16_t* dq, int BH, int N, int d, int G,
-                            int nqb, int block_l, cudaStream_t st) {
-  fold_all_kernel<<<dim3(N, BH), 64, 0, st>>>(dqt, perm, dq, N, d, G, nqb, block_l);
   return cudaGetLastError();
 }
 

@@ -80,7 +80,7 @@ template <int D>
 constexpr int epi_nc() { return D / 2 >= 32 ? 32 : D / 2; }
 
 // ------------------------------------------------------------------------------------ dK, dV
-template <int D>
+template <int D, bool CAUSAL>
 __global__ void __launch_bounds__(kThreadsB, 1)
     bwd_kv_kernel(const __grid_constant__ CUtensorMap tmQt, const __grid_constant__ CUtensorMap tmdO,
                   const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
@@ -99,7 +99,7 @@ __global__ void __launch_bounds__(kThreadsB, 1)
   const int rep = a.H / a.Hkv;
   const int b = bhkv / a.Hkv, hk = bhkv % a.Hkv;
   const int nqt = (a.N + T - 1) / T;
-  const int qt_first = a.causal ? kt : 0;  // causal: queries >= keys
+  const int qt_first = CAUSAL ? kt : 0;  // causal: queries >= keys
   const int per_head = nqt - qt_first;
   const int ntiles = rep * per_head;
   auto tile_of = [&](int n, int* bh, int* qt) {
@@ -237,7 +237,7 @@ __global__ void __launch_bounds__(kThreadsB, 1)
           const float2 x = fma2(make_float2(__uint_as_float(sr[2 * e]), __uint_as_float(sr[2 * e + 1])), sl2x2,
                                 fma2(l2, nl2e2, zero2));
           float2 p = (e & 7) >= 8 - kBwdEmu ? exp2_poly2(x) : make_float2(ex2(x.x), ex2(x.y));
-          if (a.causal) {
+          if (CAUSAL) {
             if (key > q0 + 2 * e) p.x = 0.f;
             if (key > q0 + 2 * e + 1) p.y = 0.f;
           }
@@ -288,7 +288,7 @@ __global__ void __launch_bounds__(kThreadsB, 1)
 }
 
 // ------------------------------------------------------------------------------------ dQ̃
-template <int D>
+template <int D, bool CAUSAL>
 __global__ void __launch_bounds__(kThreadsB, 1)
     bwd_q_kernel(const __grid_constant__ CUtensorMap tmQt, const __grid_constant__ CUtensorMap tmdO,
                  const __grid_constant__ CUtensorMap tmK, const __grid_constant__ CUtensorMap tmV,
@@ -306,7 +306,20 @@ __global__ void __launch_bounds__(kThreadsB, 1)
   const int qt = blockIdx.x, bh = blockIdx.y;
   const int b = bh / a.H, h = bh % a.H, bhkv = b * a.Hkv + h / (a.H / a.Hkv);
   const int nkt = (a.N + T - 1) / T;
-  const int ntiles = a.causal ? min(qt + 1, nkt) : nkt;
+  const int ntiles = CAUSAL ? min(qt + 1, nkt) : nkt;
+  // inverse permutations of the (one or two) Q blocks of this tile, for the folding epilogue
+  __shared__ uint8_t pos_s[2 * 128], pm_s[2 * 128];
+  {
+    const int qb0 = (qt * T) / a.block_l, nb = (T + a.block_l - 1) / a.block_l;
+    for (int i = threadIdx.x; i < nb * D; i += blockDim.x) {
+      const int bb = i / D, qb = qb0 + bb;
+      if (qb < a.nqb) {
+        const uint8_t c = a.perm[((size_t)bh * a.nqb + qb) * D + i % D];
+        pm_s[i] = c;
+        pos_s[bb * D + c] = (uint8_t)(i % D);
+      }
+    }
+  }
   if (threadIdx.x == 0) {
     mbar_init(&bars[BB_KV], 1);
     for (int s = 0; s < 2; ++s) {
@@ -418,7 +431,7 @@ __global__ void __launch_bounds__(kThreadsB, 1)
         for (int e = 0; e < 16; ++e) {
           const float2 x = fma2(make_float2(__uint_as_float(sr[2 * e]), __uint_as_float(sr[2 * e + 1])), sl2x2, nlse2);
           float2 p = (e & 7) >= 8 - kBwdEmu ? exp2_poly2(x) : make_float2(ex2(x.x), ex2(x.y));
-          if (a.causal) {
+          if (CAUSAL) {
             if (k0 + 2 * e > row) p.x = 0.f;
             if (k0 + 2 * e + 1 > row) p.y = 0.f;
           }
@@ -434,18 +447,43 @@ __global__ void __launch_bounds__(kThreadsB, 1)
     }
     mbar_wait(&bars[BB_DONE], 0);
     tc_fence_after();
-    float* dst = a.dqt + ((size_t)bh * a.N + row) * D + half * (D / 2);
+    // Epilogue with the fold (reading R18): dQ[r][rep_j] = Σ_{c ∈ G_j} dQ̃[r][c], 0 off the
+    // representatives. The dQ̃ rows go through shared memory (the K/V ring is idle once BB_DONE
+    // has fired: every MMA, hence every TMA load, is complete), pitch D+1 floats so that the 32
+    // rows of a warp reading one column hit 32 banks; each half then builds D/2 output columns.
+    float* rows_s = reinterpret_cast<float*>(ring);  // [128][D + 1]
+    const int rl = quad * 32 + lane;
 #pragma unroll
     for (int c = 0; c < D / 2 / NC; ++c) {
       uint32_t r[NC];
       tmem_ldn<NC>(tmem + lb + 256 + half * (D / 2) + NC * c, r);
       tmem_ld_wait();
-      if (row < a.N) {
-        float4* o = reinterpret_cast<float4*>(dst + NC * c);
 #pragma unroll
-        for (int e = 0; e < NC / 4; ++e)
-          o[e] = make_float4(__uint_as_float(r[4 * e]), __uint_as_float(r[4 * e + 1]), __uint_as_float(r[4 * e + 2]),
-                             __uint_as_float(r[4 * e + 3]));
+      for (int e = 0; e < NC; ++e) rows_s[rl * (D + 1) + half * (D / 2) + NC * c + e] = __uint_as_float(r[e]);
+    }
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    if (row < a.N) {
+      const int bb = row / a.block_l - (qt * T) / a.block_l;  // this row's Q block within the tile
+      const uint8_t* pm = pm_s + bb * D;
+      const uint8_t* pos = pos_s + bb * D;  // inverse permutation
+      uint16_t* dst = a.dq + ((size_t)bh * a.N + row) * D + half * (D / 2);
+#pragma unroll 1
+      for (int c8 = 0; c8 < D / 2; c8 += 8) {
+        uint32_t w[4];
+#pragma unroll
+        for (int e = 0; e < 8; e += 2) {
+          float v2[2];
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int col = half * (D / 2) + c8 + e + u, ps = pos[col];
+            float acc = 0.f;
+            if (ps % a.G == 0)
+              for (int g = 0; g < a.G; ++g) acc += rows_s[rl * (D + 1) + pm[ps + g]];
+            v2[u] = acc;
+          }
+          w[e / 2] = pack_bf16x2(v2[0], v2[1]);
+        }
+        *reinterpret_cast<uint4*>(dst + c8) = make_uint4(w[0], w[1], w[2], w[3]);
       }
     }
   }
@@ -457,19 +495,26 @@ __global__ void __launch_bounds__(kThreadsB, 1)
   }
 }
 
-template <int D>
-cudaError_t launch_fused_t(const BwdFusedArgs& a, cudaStream_t st) {
+template <int D, bool CAUSAL>
+cudaError_t launch_fused_c(const BwdFusedArgs& a, cudaStream_t st) {
   using C = BCfg<D>;
-  cudaError_t e = cudaFuncSetAttribute(bwd_kv_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::KV_SMEM);
+  // the causal mask is a template parameter: each kernel's elementwise loop is compiled once per
+  // flavour (no masking code in the non-causal loop) instead of depending on the compiler's
+  // loop versioning
+  cudaError_t e = cudaFuncSetAttribute(bwd_kv_kernel<D, CAUSAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::KV_SMEM);
   if (e != cudaSuccess) return e;
-  e = cudaFuncSetAttribute(bwd_q_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::Q_SMEM);
+  e = cudaFuncSetAttribute(bwd_q_kernel<D, CAUSAL>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::Q_SMEM);
   if (e != cudaSuccess) return e;
   const int nt = (a.N + T - 1) / T;
-  bwd_kv_kernel<D><<<dim3(nt, a.BHkv), kThreadsB, C::KV_SMEM, st>>>(*a.tmQt, *a.tmdO, *a.tmK, *a.tmV, a);
+  bwd_kv_kernel<D, CAUSAL><<<dim3(nt, a.BHkv), kThreadsB, C::KV_SMEM, st>>>(*a.tmQt, *a.tmdO, *a.tmK, *a.tmV, a);
   e = cudaGetLastError();
   if (e != cudaSuccess) return e;
-  bwd_q_kernel<D><<<dim3(nt, a.BH), kThreadsB, C::Q_SMEM, st>>>(*a.tmQt, *a.tmdO, *a.tmK, *a.tmV, a);
+  bwd_q_kernel<D, CAUSAL><<<dim3(nt, a.BH), kThreadsB, C::Q_SMEM, st>>>(*a.tmQt, *a.tmdO, *a.tmK, *a.tmV, a);
   return cudaGetLastError();
+}
+template <int D>
+cudaError_t launch_fused_t(const BwdFusedArgs& a, cudaStream_t st) {
+  return a.causal ? launch_fused_c<D, true>(a, st) : launch_fused_c<D, false>(a, st);
 }
 
 }  // namespace

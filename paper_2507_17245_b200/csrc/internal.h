@@ -77,16 +77,16 @@ struct BwdFusedArgs {
   const CUtensorMap *tmQt, *tmdO, *tmK, *tmV;
   const float* lse_pad;  // [BH][N_pad] (+inf past N)
   const float* D_pad;    // [BH][N_pad] (0 past N)
-  float* dqt;            // [BH][N][d] fp32 dQ̃
+  uint16_t* dq;          // [BH][N][d] bf16 dQ, folded in the dQ̃ kernel's epilogue
   uint16_t *dk, *dv;     // [BHkv][N][d] bf16 outputs
   int BH, BHkv, H, Hkv, N, N_pad, d, causal;
   float scale;
+  const uint8_t* perm;   // [BH][nqb][d] permutation of every Q block (the fold's groups)
+  int G, nqb, block_l;
 };
 cudaError_t launch_bwd_fused(const BwdFusedArgs& a, cudaStream_t st);
 // bwd.cu helpers for the fused path
 cudaError_t launch_bwd_prologue(const BwdArgs& a, const float* lse, float* lse_pad, int N_pad, cudaStream_t st);
-cudaError_t launch_fold_all(const float* dqt, const uint8_t* perm, uint16_t* dq, int BH, int N, int d, int G,
-                            int nqb, int block_l, cudaStream_t st);
 cudaError_t launch_convert_bf16(const float* src, uint16_t* dst, size_t n, cudaStream_t st);
 
 // Which kernel flavour: DISTR with (d, G, HB) or exact with d.
