@@ -541,6 +541,7 @@ int backward_fused(const void* q, const void* k, const void* v, const void* o, c
   f.lse_pad = lse_pad; f.D_pad = a.D;
   f.dq = static_cast<uint16_t*>(dq);
   f.perm = a.perm; f.G = P.G; f.nqb = P.nqb; f.block_l = P.l;
+  f.qt = a.qt; f.dout = a.dout;
   f.dk = static_cast<uint16_t*>(dk); f.dv = static_cast<uint16_t*>(dv);
   f.BH = (int)BH; f.BHkv = (int)BHkv; f.H = P.H; f.Hkv = P.Hkv; f.N = P.N; f.N_pad = (int)N_pad; f.d = P.d;
   f.causal = P.causal; f.scale = P.scale;

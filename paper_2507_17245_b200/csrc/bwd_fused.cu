@@ -48,8 +48,8 @@ struct BCfg {
   static constexpr int VEC = 1024;        // lse + D vectors of a Q tile (2 x 128 fp32)
   // kv kernel: K, V stationary + 2-stage ring of (Q̃, dO, vec)
   static constexpr int KV_SMEM = 2 * TILE + 2 * (2 * TILE + VEC) + 256 + 1024;
-  // q kernel: Q̃, dO stationary + 2-stage ring of (K, V)
-  static constexpr int Q_SMEM = 2 * TILE + 2 * (2 * TILE) + 256 + 1024;
+  // q kernel: 2-stage ring of (K, V) (Q̃, dO stationary in TMEM)
+  static constexpr int Q_SMEM = 2 * (2 * TILE) + 256 + 1024;
 };
 
 // Natural [128][d] tiles: boxes of RB columns (RB * 2-byte rows), swizzled SWIZZLE_{2 RB}B.
@@ -297,9 +297,9 @@ __global__ void __launch_bounds__(kThreadsB, 1)
   constexpr int NC = epi_nc<D>();  // epilogue TMEM columns per load
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023);
-  uint8_t* sQ = smem;
-  uint8_t* sO = sQ + C::TILE;
-  uint8_t* ring = sO + C::TILE;  // stage s: K tile, V tile
+  // Q̃ and dO are stationary A operands in TMEM (TS MMAs), so shared memory holds only the K/V
+  // ring and the tensor core reads one B tile per MMA from it.
+  uint8_t* ring = smem;  // stage s: K tile, V tile
   uint64_t* bars = reinterpret_cast<uint64_t*>(ring + 2 * (2 * C::TILE));
   uint32_t* tmem_ptr = reinterpret_cast<uint32_t*>(bars + BB_TMEM);
   const int warp = warp_id(), lane = lane_id();
@@ -307,6 +307,8 @@ __global__ void __launch_bounds__(kThreadsB, 1)
   const int b = bh / a.H, h = bh % a.H, bhkv = b * a.Hkv + h / (a.H / a.Hkv);
   const int nkt = (a.N + T - 1) / T;
   const int ntiles = CAUSAL ? min(qt + 1, nkt) : nkt;
+  // TMEM: S [0, 128), dP [128, 256), dQ̃ [256, 256 + D), Q̃ [256 + D, 256 + 3D/2), dO [.., 256 + 2D)
+  constexpr uint32_t kColQ = 256 + D, kColO = 256 + D + D / 2;
   // inverse permutations of the (one or two) Q blocks of this tile, for the folding epilogue
   __shared__ uint8_t pos_s[2 * 128], pm_s[2 * 128];
   {
@@ -321,7 +323,7 @@ __global__ void __launch_bounds__(kThreadsB, 1)
     }
   }
   if (threadIdx.x == 0) {
-    mbar_init(&bars[BB_KV], 1);
+    mbar_init(&bars[BB_KV], 256);  // the elementwise threads: Q̃ / dO rows stored into TMEM
     for (int s = 0; s < 2; ++s) {
       mbar_init(&bars[BB_FULL + s], 1);
       mbar_init(&bars[BB_EMPTY + s], 1);
@@ -344,9 +346,6 @@ __global__ void __launch_bounds__(kThreadsB, 1)
 
   if (warp == 0) {
     if (lane == 0) {
-      mbar_arrive_expect_tx(&bars[BB_KV], 2 * C::TILE);
-      load_tile<D>(sQ, &tmQt, &bars[BB_KV], qt * T, bh);
-      load_tile<D>(sO, &tmdO, &bars[BB_KV], qt * T, bh);
       for (int n = 0; n < ntiles; ++n) {
         const int s = n & 1;
         mbar_wait(&bars[BB_EMPTY + s], ((n >> 1) & 1) ^ 1);
@@ -363,7 +362,6 @@ __global__ void __launch_bounds__(kThreadsB, 1)
     constexpr uint32_t IG = make_idesc_bf16(T, D, false, true);
     mbar_wait(&bars[BB_KV], 0);
     tc_fence_after();
-    const uint32_t qb = smem_u32(sQ), ob = smem_u32(sO);
     constexpr uint32_t HROW = (T / 2) * Box<D>::ROW;
     auto issue_s = [&](int n, int hh) {  // S / dP of keys [64hh, 64hh + 64) of K/V tile n
       const int s = n & 1;
@@ -372,11 +370,11 @@ __global__ void __launch_bounds__(kThreadsB, 1)
       const uint32_t kb = smem_u32(ring + s * (2 * C::TILE)) + hh * HROW, vb = kb + C::TILE;
       if (elect_one()) {
 #pragma unroll
-        for (int kk = 0; kk < D / 16; ++kk)
-          mma_ss(tmem + 64 * hh, kmaj<D>(qb, kk), kmaj<D>(kb, kk), IS, kk > 0);
+        for (int kk = 0; kk < D / 16; ++kk)  // A = Q̃ from TMEM: K-step kk = columns [8kk, 8kk + 8)
+          mma_ts(tmem + 64 * hh, tmem + kColQ + 8 * kk, kmaj<D>(kb, kk), IS, kk > 0);
 #pragma unroll
         for (int kk = 0; kk < D / 16; ++kk)
-          mma_ss(tmem + 128 + 64 * hh, kmaj<D>(ob, kk), kmaj<D>(vb, kk), IS, kk > 0);
+          mma_ts(tmem + 128 + 64 * hh, tmem + kColO + 8 * kk, kmaj<D>(vb, kk), IS, kk > 0);
         mma_commit(&bars[BB_SFULL + hh]);
       }
       __syncwarp();
@@ -416,6 +414,28 @@ __global__ void __launch_bounds__(kThreadsB, 1)
     const float dd = a.D_pad[(size_t)bh * a.N_pad + row];
     const float2 sl2x2 = make_float2(sl2, sl2), nlse2 = make_float2(-lse2, -lse2), nd2 = make_float2(-dd, -dd),
                  zero2 = make_float2(0.f, 0.f), sc2 = make_float2(a.scale, a.scale);
+    {
+      // stationary A operands into TMEM: half 0 stores this row of Q̃, half 1 this row of dO
+      // (column c of the row = bf16 elements 2c, 2c+1; zeros past N)
+      const uint16_t* src = (half == 0 ? a.qt : a.dout) + ((size_t)bh * a.N + row) * D;
+      constexpr int W = D / 2;  // 32-bit columns per row
+      uint32_t w[W];
+#pragma unroll
+      for (int i = 0; i < W / 4; ++i) {
+        const uint4 v = row < a.N ? reinterpret_cast<const uint4*>(src)[i] : make_uint4(0u, 0u, 0u, 0u);
+        w[4 * i] = v.x; w[4 * i + 1] = v.y; w[4 * i + 2] = v.z; w[4 * i + 3] = v.w;
+      }
+      const uint32_t dst = tmem + lb + (half == 0 ? kColQ : kColO);
+      if constexpr (W >= 32) {
+#pragma unroll
+        for (int c = 0; c < W / 32; ++c) tmem_st32(dst + 32 * c, *reinterpret_cast<uint32_t(*)[32]>(&w[32 * c]));
+      } else {
+        tmem_st16(dst, *reinterpret_cast<uint32_t(*)[16]>(&w[0]));
+      }
+      tmem_st_wait();
+      tc_fence_before();
+      mbar_arrive(&bars[BB_KV]);
+    }
     for (int n = 0; n < ntiles; ++n) {
       mbar_wait(&bars[BB_SFULL + half], n & 1);
       tc_fence_after();

@@ -83,6 +83,7 @@ struct BwdFusedArgs {
   float scale;
   const uint8_t* perm;   // [BH][nqb][d] permutation of every Q block (the fold's groups)
   int G, nqb, block_l;
+  const uint16_t *qt, *dout;  // [BH][N][d] Q̃ and dO (the dQ̃ kernel's stationary TMEM operands)
 };
 cudaError_t launch_bwd_fused(const BwdFusedArgs& a, cudaStream_t st);
 // bwd.cu helpers for the fused path
