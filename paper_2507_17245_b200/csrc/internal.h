@@ -19,7 +19,7 @@ struct PrepArgs {
   uint16_t* bucket_out;  // optional export [BH][nqb][d]
   uint8_t* perm_out;     // optional export [BH][nqb][d]
   uint16_t* kt;        // [BHkv][d][N_pad] bf16 bits (nullable)
-  int n_hash_ctas;     // BH * nqb (0 = no hashing)
+  int n_hash_ctas;     // Q blocks to hash: BH * nqb (0 = no hashing); two per hash CTA
   int n_kt_ctas;       // BHkv * ceil(N/64) (0 = no K^T pass)
 };
 

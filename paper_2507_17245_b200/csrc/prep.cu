@@ -1,6 +1,6 @@
 // prep.cu — LSH / grouping pass of DistrAttention on sm_100a (one launch).
 //
-// Hash CTAs, one per (b*H + h, Q block) — §3.2-3.3:
+// Hash CTAs, two (b*H + h, Q block) units per CTA — §3.2-3.3:
 //   y[k][c] = sum_r P[k][r] * Q[r][c]   fp32 fma chain, ascending r, from +0.0f (packed
 //                                        fma.rn.f32x2: lane-wise identical to fmaf)
 //   bit_k = y > 0 ; pattern = sum bit_k << k ; bucket = inverse-Gray(pattern)
@@ -52,103 +52,107 @@ DA_DEV uint32_t inverse_gray16(uint32_t p) {
 
 DA_DEV int ilog2(int x) { return 31 - __clz(x); }
 
-// Q block staging: row pitch D+8 elements (16-byte aligned rows) shifts consecutive rows by
-// 4 banks so the 2-byte Q̂ gathers of the 4 rows a warp covers spread over the banks.
+// Hash CTAs: two Q blocks per CTA (threads [0, 128) and [128, 256)); in each half, thread t ->
+// (column pair cp = t % (D/2), projection group kg = t / (D/2)) of KPT = D/16 consecutive projection
+// rows, so one 4-byte (bf16) or 8-byte (fp32) load of the column pair per row feeds KPT FFMA2
+// (both columns, one projection row each); the projection (transposed to [r][16] in shared memory,
+// shared by both halves) is read with 16-byte loads that are uniform across the warp. Rows are
+// walked in ascending order from +0.0f (the bit-exact fma chain), the loads of 8 rows issued ahead
+// of their FMAs. Q is read straight from global memory (coalesced: a warp reads 32 consecutive
+// column pairs of one row).
 template <typename T, int D>
-constexpr int q_pitch() { return D + 16 / (int)sizeof(T); }
-
-template <typename T, int D>
-DA_DEV void hash_cta(const PrepArgs& a, int it, uint8_t* smem) {
-  constexpr int QP = q_pitch<T, D>();
-  const int QBYTES = a.block_l * QP * (int)sizeof(T);  // smem is sized for this launch's block_l
-  const int bh = it / a.nqb, qb = it - bh * a.nqb;
-  const int r0 = qb * a.block_l;
-  const int rows = min(a.block_l, a.N - r0);
+DA_DEV void hash_cta(const PrepArgs& a, int cta, uint8_t* smem) {
+  constexpr int NCP = D / 2, NKG = 256 / D, KPT = D / 16;
+  static_assert(NCP * NKG == 128, "128 threads per Q block");
+  float* proj_t = reinterpret_cast<float*>(smem);                          // [block_l][16]
+  uint8_t* parts = smem + kMaxL * 16 * 4;                                  // [2][D][NKG]
+  uint32_t* key_s = reinterpret_cast<uint32_t*>(parts + 2 * D * NKG);      // [2][D]
+  uint8_t* perm_s = reinterpret_cast<uint8_t*>(key_s + 2 * D);             // [2][D]
+  const int half = threadIdx.x >> 7, t = threadIdx.x & 127;
+  const int it = 2 * cta + half;  // Q block: bh * nqb + qb
+  const bool active = it < a.n_hash_ctas;
   const int lsh = ilog2(a.block_l);
-  T* q_s = reinterpret_cast<T*>(smem);                                 // [rows][QP]
-  float* proj_t = reinterpret_cast<float*>(smem + QBYTES);             // [r][16]
-  uint32_t* pat_s = reinterpret_cast<uint32_t*>(proj_t + a.block_l * 16);  // [NKG][D] = kThreads
-  uint32_t* key_s = pat_s + kThreads;                                  // [D]
-  uint8_t* perm_s = reinterpret_cast<uint8_t*>(key_s + D);             // [D]
-
-  // Stage the Q block (16-byte global loads, coalesced) and the transposed projection [r][16].
-  const T* qg = reinterpret_cast<const T*>(a.q) + ((size_t)bh * a.N + r0) * D;
-  constexpr int VEC = 16 / sizeof(T);
-  constexpr int VPR = D / VEC;  // vectors per row
-  for (int rb = 0; rb < rows; rb += 128) {
-    // all loads of a thread in flight before the first shared store (128-row chunks)
-    constexpr int NIT = 128 * VPR / kThreads;
-    const int cr = min(128, rows - rb);
-    uint4 v[NIT];
-#pragma unroll
-    for (int u = 0; u < NIT; ++u) {
-      const int i = threadIdx.x + u * kThreads;
-      if (i < cr * VPR) v[u] = reinterpret_cast<const uint4*>(qg + (size_t)rb * D)[i];
-    }
-#pragma unroll
-    for (int u = 0; u < NIT; ++u) {
-      const int i = threadIdx.x + u * kThreads;
-      if (i < cr * VPR) *reinterpret_cast<uint4*>(q_s + (rb + i / VPR) * QP + (i % VPR) * VEC) = v[u];
-    }
-  }
   for (int i = threadIdx.x; i < 16 * a.block_l; i += kThreads) {
     const int k = i >> lsh, r = i & (a.block_l - 1);
     proj_t[r * 16 + k] = a.proj[i];
   }
   __syncthreads();
-
-  // Projection: thread -> (column c, group of KPT consecutive projection rows).
-  constexpr int NKG = kThreads / D;  // 2 (d=128), 4 (d=64) or 8 (d=32)
-  constexpr int KPT = 16 / NKG;      // 8, 4 or 2
-  const int c = threadIdx.x % D, kg = threadIdx.x / D;
-  const int k0 = kg * KPT;
-  float2 y[KPT / 2];
+  const int bh = it / a.nqb, qb = it - bh * a.nqb;
+  if (active) {
+    const int r0 = qb * a.block_l;
+    const int rows = min(a.block_l, a.N - r0);
+    const int cp = t % NCP, kg = t / NCP, c = 2 * cp;
+    const T* qg = reinterpret_cast<const T*>(a.q) + ((size_t)bh * a.N + r0) * D + c;
+    float2 y[KPT];
 #pragma unroll
-  for (int m = 0; m < KPT / 2; ++m) y[m] = make_float2(0.0f, 0.0f);
-  for (int r = 0; r < rows; ++r) {
-    const float qv = load_f<T>(q_s + r * QP + c);
-    const float2 qq = make_float2(qv, qv);
-    if constexpr (KPT == 2) {
-      const float2 pa = *reinterpret_cast<const float2*>(proj_t + r * 16 + k0);
-      y[0] = fma2(pa, qq, y[0]);
-    } else {
-#pragma unroll
-      for (int m = 0; m < KPT / 4; ++m) {
-        const float4 pa = *reinterpret_cast<const float4*>(proj_t + r * 16 + k0 + 4 * m);
-        y[2 * m] = fma2(make_float2(pa.x, pa.y), qq, y[2 * m]);
-        y[2 * m + 1] = fma2(make_float2(pa.z, pa.w), qq, y[2 * m + 1]);
+    for (int m = 0; m < KPT; ++m) y[m] = make_float2(0.0f, 0.0f);
+    auto load_pair = [&](int r) -> float2 {
+      if constexpr (sizeof(T) == 2) {
+        const uint32_t w = *reinterpret_cast<const uint32_t*>(qg + (size_t)r * D);
+        return make_float2(__uint_as_float(w << 16), __uint_as_float(w & 0xFFFF0000u));
+      } else {
+        return *reinterpret_cast<const float2*>(qg + (size_t)r * D);
       }
-    }
-  }
-  uint32_t part = 0;
+    };
+    auto fma_row = [&](int r, float2 qq) {
+      const float* pr = proj_t + r * 16 + kg * KPT;
+      float pk[KPT];
+      if constexpr (KPT >= 4) {
 #pragma unroll
-  for (int m = 0; m < KPT / 2; ++m) {
-    part |= (y[m].x > 0.0f ? 1u : 0u) << (k0 + 2 * m);
-    part |= (y[m].y > 0.0f ? 1u : 0u) << (k0 + 2 * m + 1);
+        for (int v = 0; v < KPT / 4; ++v) {
+          const float4 p4 = *reinterpret_cast<const float4*>(pr + 4 * v);
+          pk[4 * v] = p4.x; pk[4 * v + 1] = p4.y; pk[4 * v + 2] = p4.z; pk[4 * v + 3] = p4.w;
+        }
+      } else {
+        const float2 p2 = *reinterpret_cast<const float2*>(pr);
+        pk[0] = p2.x; pk[1] = p2.y;
+      }
+#pragma unroll
+      for (int m = 0; m < KPT; ++m) y[m] = fma2(make_float2(pk[m], pk[m]), qq, y[m]);
+    };
+    int r = 0;
+    for (; r + 8 <= rows; r += 8) {
+      float2 qv[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) qv[j] = load_pair(r + j);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) fma_row(r + j, qv[j]);
+    }
+    for (; r < rows; ++r) fma_row(r, load_pair(r));
+    uint32_t pa = 0, pb = 0;
+#pragma unroll
+    for (int m = 0; m < KPT; ++m) {
+      pa |= (y[m].x > 0.0f ? 1u : 0u) << m;
+      pb |= (y[m].y > 0.0f ? 1u : 0u) << m;
+    }
+    parts[(half * D + c) * NKG + kg] = (uint8_t)pa;
+    parts[(half * D + c + 1) * NKG + kg] = (uint8_t)pb;
   }
-  pat_s[kg * D + c] = part;
   __syncthreads();
-
-  if (threadIdx.x < D) {
+  if (active && t < D) {
     uint32_t pattern = 0;
 #pragma unroll
-    for (int g = 0; g < NKG; ++g) pattern |= pat_s[g * D + threadIdx.x];
+    for (int g = 0; g < NKG; ++g) pattern |= (uint32_t)parts[(half * D + t) * NKG + g] << (KPT * g);
     const uint32_t bucket = inverse_gray16(pattern);
-    key_s[threadIdx.x] = (bucket << 8) | (uint32_t)threadIdx.x;  // unique (bucket, column) key
-    if (a.bucket_out) a.bucket_out[(size_t)it * D + threadIdx.x] = (uint16_t)bucket;
+    key_s[half * D + t] = (bucket << 8) | (uint32_t)t;  // unique (bucket, column) key
+    if (a.bucket_out) a.bucket_out[(size_t)it * D + t] = (uint16_t)bucket;
   }
   __syncthreads();
-  if (threadIdx.x < D) {
-    const uint32_t mine = key_s[threadIdx.x];
+  if (active && t < D) {
+    const uint32_t mine = key_s[half * D + t];
+    const uint4* ks = reinterpret_cast<const uint4*>(key_s + half * D);
     int rank = 0;
-#pragma unroll 16
-    for (int j = 0; j < D; ++j) rank += key_s[j] < mine ? 1 : 0;
-    perm_s[rank] = (uint8_t)threadIdx.x;
+#pragma unroll 8
+    for (int j = 0; j < D / 4; ++j) {
+      const uint4 k4 = ks[j];
+      rank += (k4.x < mine ? 1 : 0) + (k4.y < mine ? 1 : 0) + (k4.z < mine ? 1 : 0) + (k4.w < mine ? 1 : 0);
+    }
+    perm_s[half * D + rank] = (uint8_t)t;
   }
   __syncthreads();
-  if (threadIdx.x < D) {
-    if (a.perm_ws) a.perm_ws[(size_t)it * D + threadIdx.x] = perm_s[threadIdx.x];
-    if (a.perm_out) a.perm_out[(size_t)it * D + threadIdx.x] = perm_s[threadIdx.x];
+  if (active && t < D) {
+    if (a.perm_ws) a.perm_ws[(size_t)it * D + t] = perm_s[half * D + t];
+    if (a.perm_out) a.perm_out[(size_t)it * D + t] = perm_s[half * D + t];
   }
 }
 
@@ -223,11 +227,11 @@ __global__ void __launch_bounds__(kThreads) prep_kernel(const PrepArgs a) {
   // their in-CTA LSH prologue, which reads only Q) while this grid runs; it waits on the grid
   // dependency before its first K^T load.
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  const int bid = blockIdx.x;
-  if (bid < a.n_hash_ctas)
+  const int bid = blockIdx.x, nh = (a.n_hash_ctas + 1) / 2;  // two Q blocks per hash CTA
+  if (bid < nh)
     hash_cta<T, D>(a, bid, smem);
   else
-    kt_cta<T, D>(a, bid - a.n_hash_ctas, smem);
+    kt_cta<T, D>(a, bid - nh, smem);
 }
 
 __global__ void convert_kernel(const float* __restrict__ src, uint16_t* __restrict__ dst, size_t n) {
@@ -237,15 +241,14 @@ __global__ void convert_kernel(const float* __restrict__ src, uint16_t* __restri
 
 template <typename T, int D>
 size_t prep_smem_bytes(int block_l) {  // block_l = 0: no hash CTAs in this launch
-  const size_t q = (size_t)block_l * q_pitch<T, D>() * sizeof(T);
-  const size_t hash = block_l ? q + block_l * 16 * 4 + kThreads * 4 + D * 4 + D + 16 : 0;
+  const size_t hash = block_l ? kMaxL * 16 * 4 + 2 * D * (256 / D) + 2 * D * 4 + 2 * D : 0;
   const size_t kt = 64 * D * 2;
   return std::max(hash, kt);
 }
 
 template <typename T, int D>
 cudaError_t launch_prep_t(const PrepArgs& a, cudaStream_t st) {
-  const int grid = a.n_hash_ctas + a.n_kt_ctas;
+  const int grid = (a.n_hash_ctas + 1) / 2 + a.n_kt_ctas;
   const size_t smem = prep_smem_bytes<T, D>(a.n_hash_ctas ? a.block_l : 0);
   cudaError_t e = cudaFuncSetAttribute(prep_kernel<T, D>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
