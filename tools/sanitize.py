@@ -20,5 +20,13 @@ da.distr_attn_fwd_ex(qf, kf, vf, block_l=64, group_size=2)
 g = torch.Generator(device="cuda").manual_seed(1)
 do = torch.randn(q.shape, generator=g, device="cuda").bfloat16()
 da.distr_attn_bwd_ex(q, k, v, o, do, lse, block_l=128, group_size=2, causal=True)
+# non-causal backward at d = 64 and d = 32 (the other template instances of the fused kernels)
+for dd, seed in ((64, 6), (32, 7)):
+    cb = Config("s", 1, 2, 2, 260, dd, 128, 2, False, "bf16", seed)
+    qb, kb, vb = make_qkv(cb, device="cuda")
+    lb = torch.empty((1, 2, 260), device="cuda")
+    ob = da.distr_attn_fwd_ex(qb, kb, vb, block_l=128, group_size=2, lse=lb)
+    da.distr_attn_bwd_ex(qb, kb, vb, ob, torch.randn(qb.shape, generator=g, device="cuda").bfloat16(), lb,
+                         block_l=128, group_size=2)
 torch.cuda.synchronize()
 print("sanitize workload done")
