@@ -6,8 +6,8 @@
 //   dK = scale · dŜᵀ Q̃ already holds dK̂ copied onto every group member, and dQ̃ = scale · dŜ K
 //   folds onto the representatives: dQ[r][rep_j] = Σ_{c ∈ G_j} dQ̃[r][c] (zero elsewhere).
 //
-// Kernels: qtilde (Q̃ rows + D[r] = Σ dO∘O), lse_pad (the forward's LSE padded with +inf to whole
-// 128-row tiles). The fold dQ̃ -> dQ runs in the dQ̃ kernel's epilogue (bwd_fused.cu).
+// Kernels: qtilde (Q̃ rows + −D[r] = −Σ dO∘O), lse_pad (−log2e × the forward's LSE, padded with −inf
+// to whole 128-row tiles). The fold dQ̃ -> dQ runs in the dQ̃ kernel's epilogue (bwd_fused.cu).
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -52,7 +52,7 @@ __global__ void __launch_bounds__(256) qtilde_kernel(const BwdArgs a) {
     }
 #pragma unroll
     for (int m = 1; m < CPR; m <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, m);
-    if (ch == 0 && r < rows) a.D[(size_t)bh * a.Dstride + r0 + r] = acc;
+    if (ch == 0 && r < rows) a.D[(size_t)bh * a.Dstride + r0 + r] = -acc;  // stored negated: the kernels add it
   }
   __syncthreads();
   for (int c = threadIdx.x; c < D; c += blockDim.x) rep_s[c] = perm[(inv_s[c] / a.G) * a.G];
@@ -73,7 +73,8 @@ __global__ void lse_pad_kernel(const float* lse, float* out, int BH, int N, int 
   const size_t total = (size_t)BH * N_pad;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
     const size_t bh = i / N_pad, r = i % N_pad;
-    out[i] = r < (size_t)N ? lse[bh * N + r] : __int_as_float(0x7f800000);  // +inf: P = 0 past N
+    // −lse·log2e, the addend of the backward kernels' exp2 argument; −inf past N: P = 0 there
+    out[i] = r < (size_t)N ? -lse[bh * N + r] * 1.4426950408889634f : __int_as_float(0xff800000);
   }
 }
 

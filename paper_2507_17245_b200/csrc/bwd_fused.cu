@@ -207,9 +207,8 @@ __global__ void __launch_bounds__(kThreadsB, 1)
     const int half = (warp - 4) >> 2, quad = warp & 3;
     const int key = kt * T + quad * 32 + lane;  // this thread's key row (TMEM lane)
     const uint32_t lb = (uint32_t)(quad * 32) << 16;
-    const float sl2 = a.scale * 1.4426950408889634f, l2e = 1.4426950408889634f;
-    const float2 sl2x2 = make_float2(sl2, sl2), nl2e2 = make_float2(-l2e, -l2e), zero2 = make_float2(0.f, 0.f),
-                 sc2 = make_float2(a.scale, a.scale);
+    const float sl2 = a.scale * 1.4426950408889634f;
+    const float2 sl2x2 = make_float2(sl2, sl2), zero2 = make_float2(0.f, 0.f), sc2 = make_float2(a.scale, a.scale);
     for (int n = 0; n < ntiles; ++n) {
       const int s = n & 1;
       int bh, qt;
@@ -230,23 +229,30 @@ __global__ void __launch_bounds__(kThreadsB, 1)
         const float* dv = vec + 128 + 64 * half + 32 * c2;
         uint32_t pk[16], dk2[16];
 #pragma unroll
-        for (int e = 0; e < 16; ++e) {
-          // x = S·scale·log2e − lse·log2e (FFMA2), exp2 on MUFU or, for kBwdEmu of every 8 pairs,
-          // the FMA-pipe polynomial (the elementwise phase is MUFU-bound at d <= 64)
-          const float2 l2 = *reinterpret_cast<const float2*>(lv + 2 * e);
-          const float2 x = fma2(make_float2(__uint_as_float(sr[2 * e]), __uint_as_float(sr[2 * e + 1])), sl2x2,
-                                fma2(l2, nl2e2, zero2));
-          float2 p = (e & 7) >= 8 - kBwdEmu ? exp2_poly2(x) : make_float2(ex2(x.x), ex2(x.y));
-          if (CAUSAL) {
-            if (key > q0 + 2 * e) p.x = 0.f;
-            if (key > q0 + 2 * e + 1) p.y = 0.f;
+        for (int e4 = 0; e4 < 8; ++e4) {
+          // the tile's −lse·log2e and −D are the same for every lane (key): one 16-byte broadcast
+          // load per 4 queries of each (shared-memory wavefronts are the dK/dV kernel's
+          // co-bottleneck with the tensor core's operand reads)
+          const float4 nl4 = *reinterpret_cast<const float4*>(lv + 4 * e4);
+          const float4 nd4 = *reinterpret_cast<const float4*>(dv + 4 * e4);
+#pragma unroll
+          for (int h2 = 0; h2 < 2; ++h2) {
+            const int e = 2 * e4 + h2;
+            const float2 nl2 = h2 ? make_float2(nl4.z, nl4.w) : make_float2(nl4.x, nl4.y);
+            const float2 nd2 = h2 ? make_float2(nd4.z, nd4.w) : make_float2(nd4.x, nd4.y);
+            // x = S·scale·log2e − lse·log2e (FFMA2), exp2 on MUFU or, for kBwdEmu of every 8
+            // pairs, the FMA-pipe polynomial (the elementwise phase is MUFU-bound at d <= 64)
+            const float2 x = fma2(make_float2(__uint_as_float(sr[2 * e]), __uint_as_float(sr[2 * e + 1])), sl2x2, nl2);
+            float2 p = (e & 7) >= 8 - kBwdEmu ? exp2_poly2(x) : make_float2(ex2(x.x), ex2(x.y));
+            if (CAUSAL) {
+              if (key > q0 + 2 * e) p.x = 0.f;
+              if (key > q0 + 2 * e + 1) p.y = 0.f;
+            }
+            const float2 g = fadd2(make_float2(__uint_as_float(pr[2 * e]), __uint_as_float(pr[2 * e + 1])), nd2);
+            const float2 ds = fma2(fma2(p, g, zero2), sc2, zero2);
+            pk[e] = pack_bf16x2(p.x, p.y);
+            dk2[e] = pack_bf16x2(ds.x, ds.y);
           }
-          const float2 d2 = *reinterpret_cast<const float2*>(dv + 2 * e);
-          const float2 g = fadd2(make_float2(__uint_as_float(pr[2 * e]), __uint_as_float(pr[2 * e + 1])),
-                                 make_float2(-d2.x, -d2.y));
-          const float2 ds = fma2(fma2(p, g, zero2), sc2, zero2);
-          pk[e] = pack_bf16x2(p.x, p.y);
-          dk2[e] = pack_bf16x2(ds.x, ds.y);
         }
         // into this half's own columns (no other warp reads them): no race with the other half
         tmem_st16(tmem + lb + 64 * half + 16 * c2, pk);
@@ -410,9 +416,9 @@ __global__ void __launch_bounds__(kThreadsB, 1)
     const int row = qt * T + quad * 32 + lane;
     const uint32_t lb = (uint32_t)(quad * 32) << 16;
     const float sl2 = a.scale * 1.4426950408889634f;
-    const float lse2 = a.lse_pad[(size_t)bh * a.N_pad + row] * 1.4426950408889634f;
-    const float dd = a.D_pad[(size_t)bh * a.N_pad + row];
-    const float2 sl2x2 = make_float2(sl2, sl2), nlse2 = make_float2(-lse2, -lse2), nd2 = make_float2(-dd, -dd),
+    const float nlse2_r = a.lse_pad[(size_t)bh * a.N_pad + row];  // −lse·log2e
+    const float ndd = a.D_pad[(size_t)bh * a.N_pad + row];         // −D
+    const float2 sl2x2 = make_float2(sl2, sl2), nlse2 = make_float2(nlse2_r, nlse2_r), nd2 = make_float2(ndd, ndd),
                  zero2 = make_float2(0.f, 0.f), sc2 = make_float2(a.scale, a.scale);
     {
       // stationary A operands into TMEM: half 0 stores this row of Q̃, half 1 this row of dO

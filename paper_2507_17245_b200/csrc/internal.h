@@ -75,8 +75,8 @@ struct BwdArgs {
 // [BHkv][N][d], all min(d, 64)-column SWIZZLE_{2 min(d, 64)}B boxes of 128 rows.
 struct BwdFusedArgs {
   const CUtensorMap *tmQt, *tmdO, *tmK, *tmV;
-  const float* lse_pad;  // [BH][N_pad] (+inf past N)
-  const float* D_pad;    // [BH][N_pad] (0 past N)
+  const float* lse_pad;  // [BH][N_pad] −lse·log2e (−inf past N)
+  const float* D_pad;    // [BH][N_pad] −D (0 past N)
   uint16_t* dq;          // [BH][N][d] bf16 dQ, folded in the dQ̃ kernel's epilogue
   uint16_t *dk, *dv;     // [BHkv][N][d] bf16 outputs
   int BH, BHkv, H, Hkv, N, N_pad, d, causal;
