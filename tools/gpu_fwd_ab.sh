@@ -1,0 +1,21 @@
+#!/bin/bash
+# Forward A/B: quick parity + CTA timelines + C5 bench (kernel-only) + C4-16k sweep rows for the
+# in-tree build and each tools/exp variant, alternating (default, v1, default, v1, ...).
+O=gpurun_out/fwd_ab; mkdir -p $O
+[ -x tools/mb/softmax2 ] && ./tools/mb/softmax2 > $O/softmax2.txt 2>&1
+cp paper_2507_17245_b200/libdistr_attn.so /tmp/lib_default.so
+use() { if [ $1 = default ]; then cp /tmp/lib_default.so paper_2507_17245_b200/libdistr_attn.so; else cp tools/exp/lib_$1.so paper_2507_17245_b200/libdistr_attn.so; fi; }
+for v in "$@"; do
+  use $v
+  timeout -s KILL 180 python tools/quick.py > $O/quick_$v.log 2>&1; echo "rc=$?" >> $O/quick_$v.log
+  timeout -s KILL 60 python tools/trace.py distr > $O/trace_distr_$v.log 2>&1
+  timeout -s KILL 60 python tools/trace.py exact > $O/trace_exact_$v.log 2>&1
+done
+for rep in 1 2; do
+  for v in default "$@"; do
+    use $v
+    timeout -s KILL 600 python bench.py --no-e2e --no-cpu --no-parity --steps 10 > $O/bench_${v}_$rep.log 2>&1
+    timeout -s KILL 300 python tools/sweep.py --no-error --only "C4 N=16384,C4 N=4096" > $O/sweep_${v}_$rep.json 2>&1
+  done
+done
+use default
