@@ -135,10 +135,11 @@ int distr_attn_global_fwd_ex(const void* q, const void* k, const void* v, void* 
  * LSE (da_params.lse of the forward call, [B, H, N] fp32), and dout = dL/dout; outputs dq
  * [B,H,N,d], dk, dv [B,H_kv,N,d] (bf16, overwritten). Same params as the forward (block_l,
  * group_size, seed select the grouping; causal, scale; group_size = 1 gives exact attention
- * gradients). bf16 only, d in {32, 64, 128}: six launches of this library's kernels — the prep
+ * gradients). bf16 only, d in {32, 64, 128}: five launches of this library's kernels — the prep
  * hash (perm per Q block), Q̃ (every column replaced by its group representative) + D =
- * rowsum(dO*O), the LSE padded with +inf, the fused tcgen05 dK/dV kernel, the fused tcgen05 dQ̃
- * kernel, and the fold of dQ̃ onto the representative columns; stream-ordered, no host sync.
+ * rowsum(dO*O), the LSE scaled by -log2(e) and padded with -inf, the fused tcgen05 dK/dV kernel,
+ * and the fused tcgen05 dQ̃ kernel, whose epilogue folds dQ̃ onto the representative columns and
+ * writes dq; stream-ordered, no host sync.
  * Workspace: the caller's (p->workspace, >= distr_attn_bwd_workspace_size(p) bytes) or
  * stream-ordered library scratch. */
 int distr_attn_bwd_ex(const void* q, const void* k, const void* v, const void* out, const void* dout,

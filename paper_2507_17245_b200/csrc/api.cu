@@ -267,11 +267,11 @@ int current_device(int* dev) {
 }
 
 // Share of exp2 pairs (out of 8) evaluated by polynomial on the FMA pipe instead of MUFU.EX2.
-// Measured on B200 (profiles/r01_v4): the exp phase of a tile is MUFU-bound
-// (16 ex2/clk/SM); moving 2/8 of the pairs to the FMA pipe shortens it by ~10 % and helps the
-// distr kernel, whose tensor-core block is shorter than the softmax; the exact kernel is then
-// co-bound by its longer tensor block and loses (power draw), so it keeps 0. DA_EMU (distr) and
-// DA_EMU_EXACT (exact) override (0, 2, 3, 4) for tuning.
+// The exp phase of a tile is MUFU-bound (16 ex2/clk/SM); moving 2/8 of the pairs to the FMA pipe
+// shortens it. With the round-2 alternating softmax the exact kernel was best at 0 (its longer
+// tensor block co-bound it, profiles/r01_v9/emu_ab); with the ping-pong softmax (one warp per SM
+// sub-partition per tile) both flavours are best at 2. DA_EMU (distr) and DA_EMU_EXACT (exact)
+// override (0, 2, 3, 4) for tuning.
 int default_emu(const Plan& P, bool distr) {
   static const int env[2] = {[] {
                                const char* e = getenv("DA_EMU_EXACT");
@@ -283,7 +283,9 @@ int default_emu(const Plan& P, bool distr) {
                              }()};
   (void)P;
   if (env[distr ? 1 : 0] >= 0) return env[distr ? 1 : 0];
-  return distr ? 2 : 0;
+  // ping-pong softmax (attn.cu, the default): EMU = 2 is the best setting of both flavours
+  // (C5, alternating runs on one box, profiles/r02_v6/fwd_ab2: exact EMU 0 / 2 = 118.8 / 117.7 ms)
+  return 2;
 }
 
 // ---------------------------------------------------------------------------- forward

@@ -12,12 +12,15 @@
 //                 S_t  = A_t · B_t^T        (M=128, N=128, K = d or DR = HB*d/G*; fp32 in TMEM)
 //                 O_t += P_t · V            (A = P_t bf16 read from TMEM, B = V MN-major, N = d)
 //   warp 2      TMA producer of the V ring (SW128); warp 3 idle.
-//   warps 4-11  softmax: all 8 warps work on ONE tile at a time, alternating tiles in the MMA's
-//               order, so tile t's exp phase overlaps the tensor core's work on tile 1-t. Warps
-//               w and w+4 own the same 32 TMEM lanes (query rows) and split the 128 key columns;
-//               row max combined through smem; lazy O rescale (only when the running max grows
-//               by > 2^8); exp2 on MUFU plus an FMA-pipe polynomial for EMU/8 of the pairs; P ->
-//               TMEM (bf16) in 8-column chunks; O / l epilogue.
+//   warps 4-11  softmax, two warpgroups (DA_PINGPONG = 1, the default): warps 4-7 own Q tile 0,
+//               warps 8-11 tile 1; thread = query row = TMEM lane with all 128 keys of a tile, so
+//               no row-max exchange, and one tile's S load / max / hand-off overlaps the other
+//               tile's exps. Lazy O rescale (only when the running max grows by > 2^8); exp2 on
+//               MUFU for the first pass over the row and the FMA-pipe polynomial for EMU/8 of the
+//               pairs in a second pass (DA_EXP_SPLIT); P -> TMEM (bf16); O / l epilogue.
+//               DA_PINGPONG = 0 keeps the round-2 layout: all 8 warps on one tile at a time,
+//               alternating tiles, two warps per row splitting the keys (row max exchanged
+//               through shared memory).
 //   warps 12-15 (distr) fusion: K̂_t^T[j][key] = sum_{c in G_j} K^T[c][key] with each tile's own
 //               permutation(s) — Eq. 2 with the block-wise grouping of §3.3 (P:306:
 //               "the rows of a K block are grouped depending on which Q block is multiplied by").
@@ -45,6 +48,26 @@
 #endif
 #ifndef DA_EMU_SPREAD
 #define DA_EMU_SPREAD 0
+#endif
+// Experimental (off): FA4-style ping-pong softmax — warps 4-7 own Q tile 0, warps 8-11 tile 1,
+// thread = query row with all 128 keys of a tile (no row-max exchange), so one tile's S load / max
+// overlaps the other tile's exps.
+#ifndef DA_PINGPONG
+#define DA_PINGPONG 1
+#endif
+// DA_PINGPONG = 2 additionally computes S_t(i+1) in two 64-key halves: P_t(i) goes to the upper
+// 64 columns of S_t, so the lower half of S_t(i+1) is issued as soon as the tile's softmax has
+// loaded S_t(i) (B_SLD), and only the upper half waits for PV_t(i).
+// DA_EXP_SPLIT (ping-pong softmax): the MUFU pairs of a row first, the FMA-pipe polynomial pairs
+// after them (tools/mb/softmax2.cu: 8 % shorter exp phase with one warp per sub-partition).
+#ifndef DA_EXP_SPLIT
+#define DA_EXP_SPLIT 1
+#endif
+// DA_PV_SPLIT (ping-pong, with DA_EXP_SPLIT): the softmax finishes keys 0-63 of a row first and
+// signals B_PHALF, so PV over those keys runs during the second half's exps and only PV over keys
+// 64-127 (then S_t(i+1)) remains on the P -> S chain.
+#ifndef DA_PV_SPLIT
+#define DA_PV_SPLIT 1
 #endif
 // Consumer-release barriers (P ready, K̂ ready, K stage free, Q̂ built) take one arrival per warp
 // (lane 0 after __syncwarp) instead of one per thread. Measured on B200: no gain (the MMA warp's
@@ -140,7 +163,9 @@ enum {
   B_OFULL = 21,   // +t
   B_QHAT = 23,    // distr: Q̂ of both tiles built in sA (kWorkers hashing threads arrive)
   B_TMEMPTR = 24,
-  B_COUNT = 25
+  B_SLD = 25,     // +t: ping-pong split S (DA_PINGPONG = 2): the tile's softmax has loaded S_t(i)
+  B_PHALF = 27,   // +t: DA_PV_SPLIT: P_t(i) of keys 0-63 is in TMEM
+  B_COUNT = 29
 };
 
 // Release arrival of a whole warp: every lane's prior writes (and fences) are ordered before lane
@@ -392,8 +417,14 @@ __global__ void __launch_bounds__(threads_of<DISTR>(), 1)
         mbar_init(&bars[B_KHEMPTY + 2 * t + st], 1);
       }
       mbar_init(&bars[B_SFULL + t], 1);
+#if DA_PINGPONG
+      mbar_init(&bars[B_PFULL + t], kSoftmaxThreads / 2 / kArrive);  // one softmax warpgroup per tile
+#else
       mbar_init(&bars[B_PFULL + t], kSoftmaxThreads / kArrive);
+#endif
       mbar_init(&bars[B_OFULL + t], 1);
+      mbar_init(&bars[B_SLD + t], kSoftmaxThreads / 2);
+      mbar_init(&bars[B_PHALF + t], kSoftmaxThreads / 2);
     }
     fence_mbar_init();
     // A operand, issued before anything else: exact -> Q tiles straight into sA; distr -> natural
@@ -528,19 +559,45 @@ __global__ void __launch_bounds__(threads_of<DISTR>(), 1)
       };
       auto issue_pv = [&](int t, int j) {
         const int s = j % NS;
+#if DA_PV_SPLIT
+        // keys 0-63 of P_t(j) as soon as the softmax has stored them
+        mbar_wait(&bars[B_PHALF + t], j & 1);
+        if (t == 0 || nkt_t[0] <= j) mbar_wait(&bars[B_VFULL + s], (j / NS) & 1);
+        tc_fence_after();
+        {
+          const uint32_t v_base = smem_u32(sV + s * C::V_BYTES);
+          const uint32_t p_tmem = tmem + kColS + 128u * t;
+          uint64_t vd[BN / 32];
+#pragma unroll
+          for (int kk = 0; kk < BN / 32; ++kk)
+            vd[kk] = make_sdesc(v_base + kk * 16 * C::RB * 2, BN * C::RB * 2, 8 * C::RB * 2, C::RB == 64 ? kSw128 : kSw64);
+          if (elect_one()) {
+#pragma unroll
+            for (int kk = 0; kk < BN / 32; ++kk)
+              mma_ts(tmem + (uint32_t)(t * D), p_tmem + kk * 8, vd[kk], IDESC_PV, (j > 0 || kk > 0) ? 1u : 0u);
+          }
+          __syncwarp();
+        }
+        mbar_wait(&bars[B_PFULL + t], j & 1);
+        if (lead) DA_TRACE(8 + t, j, true);
+        tc_fence_after();
+        constexpr int kk0 = BN / 32;  // the second half's K-steps
+#else
         mbar_wait(&bars[B_PFULL + t], j & 1);
         if (lead) DA_TRACE(8 + t, j, true);
         if (t == 0 || nkt_t[0] <= j) mbar_wait(&bars[B_VFULL + s], (j / NS) & 1);
         tc_fence_after();
+        constexpr int kk0 = 0;
+#endif
         const uint32_t v_base = smem_u32(sV + s * C::V_BYTES);
-        const uint32_t p_tmem = tmem + kColS + 128u * t;
+        const uint32_t p_tmem = tmem + kColS + 128u * t + (DA_PINGPONG == 2 ? 64u : 0u);
         uint64_t vd[BN / 16];
 #pragma unroll
         for (int kk = 0; kk < BN / 16; ++kk)  // V as the MN-major B operand: RB-column blocks (LBO), 8-key groups (SBO)
           vd[kk] = make_sdesc(v_base + kk * 16 * C::RB * 2, BN * C::RB * 2, 8 * C::RB * 2, C::RB == 64 ? kSw128 : kSw64);
         if (elect_one()) {
 #pragma unroll
-          for (int kk = 0; kk < BN / 16; ++kk)
+          for (int kk = kk0; kk < BN / 16; ++kk)
             mma_ts(tmem + (uint32_t)(t * D), p_tmem + kk * 8, vd[kk], IDESC_PV, (j > 0 || kk > 0) ? 1u : 0u);
           if (j == nkt_t[t] - 1) mma_commit(&bars[B_OFULL + t]);
         }
@@ -560,6 +617,69 @@ __global__ void __launch_bounds__(threads_of<DISTR>(), 1)
 
       mbar_wait(&bars[DISTR ? B_QHAT : B_Q], 0);
       tc_fence_after();
+#if DA_PINGPONG == 2
+      constexpr uint32_t IDESC_SH = make_idesc_bf16(BM, BN / 2, false, DISTR);
+      // half h of S_t(i): keys [64h, 64h + 64) -> columns [64h, 64h + 64) of S_t
+      auto issue_sh = [&](int t, int i, int h) {
+        const int s = i % NS;
+        const int tk = C::SHARED ? 0 : t;
+        if (h == 0) {
+          if (DISTR)
+            mbar_wait(&bars[B_KHFULL + 2 * tk + i % NKH], (i / NKH) & 1);
+          else if (t == 0 || nkt_t[0] <= i)
+            mbar_wait(&bars[B_KFULL + s], (i / NS) & 1);
+          tc_fence_after();
+        }
+        const uint32_t d_s = tmem + kColS + 128u * t + 64u * h;
+        uint64_t ad[KS], bd[KS];
+#pragma unroll
+        for (int kk = 0; kk < KS; ++kk) {
+          ad[kk] = make_sdesc(a_base + t * C::A_BYTES + (kk / kpb) * C::A_BOX_BYTES + (kk % kpb) * 32, 16,
+                              8 * C::A_SW, C::A_LAYOUT);
+          if (DISTR)  // 64-key block h of K̂^T
+            bd[kk] = make_sdesc(smem_u32(sKh + (tk * NKH + i % NKH) * C::KH_BYTES) + kk * 2048 + h * (C::DR * 128),
+                                C::DR * 128, 1024, kSw128);
+          else  // key rows [64h, 64h + 64) of the K tile
+            bd[kk] = make_sdesc(smem_u32(sK + s * C::K_BYTES) + (kk / kpb) * C::A_BOX_BYTES + (kk % kpb) * 32 +
+                                    h * 64 * C::A_SW,
+                                16, 8 * C::A_SW, C::A_LAYOUT);
+        }
+        if (elect_one()) {
+#pragma unroll
+          for (int kk = 0; kk < KS; ++kk) mma_ss(d_s, ad[kk], bd[kk], IDESC_SH, kk > 0 ? 1u : 0u);
+          if (h == 1) {
+            mma_commit(&bars[B_SFULL + t]);
+            if (DISTR && (!C::SHARED || t == 1 || i >= nkt_t[1])) mma_commit(&bars[B_KHEMPTY + 2 * tk + i % NKH]);
+          }
+        }
+        __syncwarp();
+        if (lead && h == 1) DA_TRACE(6 + t, i, true);
+      };
+#pragma unroll
+      for (int t = 0; t < 2; ++t)
+        if (0 < nkt_t[t]) {
+          issue_sh(t, 0, 0);
+          issue_sh(t, 0, 1);
+        }
+      if (nk > 0) release_k(0);
+      for (int i = 0; i < nk; ++i) {
+        // lower halves of step i+1 as soon as each tile's softmax holds S_t(i) in registers
+#pragma unroll
+        for (int t = 0; t < 2; ++t)
+          if (i + 1 < nkt_t[t]) {
+            mbar_wait(&bars[B_SLD + t], i & 1);
+            issue_sh(t, i + 1, 0);
+          }
+#pragma unroll
+        for (int t = 0; t < 2; ++t)
+          if (i < nkt_t[t]) {
+            issue_pv(t, i);
+            if (t == 1 || !(i < nkt_t[1])) release_v(i);
+            if (i + 1 < nkt_t[t]) issue_sh(t, i + 1, 1);  // upper half: in-order after PV_t(i) read P_t(i)
+          }
+        if (i + 1 < nk) release_k(i + 1);
+      }
+#else
       for (int i = 0; i < nk; ++i) {
         // tile 0: PV_0(i-1) then S_0(i)   (S_0(i) overwrites P_0(i-1): in-order after the PV)
         if (i >= 1 && i - 1 < nkt_t[0]) issue_pv(0, i - 1);
@@ -575,9 +695,181 @@ __global__ void __launch_bounds__(threads_of<DISTR>(), 1)
       if (nk - 1 < nkt_t[0]) issue_pv(0, nk - 1);
       if (nk - 1 < nkt_t[1]) issue_pv(1, nk - 1);
       release_v(nk - 1);
+#endif
     }
   }  // warp 3 idle
   } else if (warp < 4 + kSoftmaxWarps) {
+#if DA_PINGPONG
+    static_assert(kSplit == 2, "ping-pong uses the 8 softmax warps as two warpgroups");
+    if (DISTR)
+      asm volatile("setmaxnreg.inc.sync.aligned.u32 184;");
+    else
+      asm volatile("setmaxnreg.inc.sync.aligned.u32 208;");
+    {
+      const int t = (warp - 4) >> 2;
+      const int nkt = nkt_t[t];
+      const int row = (warp & 3) * 32 + lane;
+      const uint32_t lane_base = (uint32_t)((warp & 3) * 32) << 16;
+      const uint32_t tS = tmem + lane_base + kColS + 128u * t;
+      const uint32_t tO = tmem + lane_base + (uint32_t)(t * D);
+      const int q0 = (qt0 + t) * BM;
+      const int q_row = q0 + row;
+      const float sl2 = args.scale_log2;
+      const bool tr = row == 0;
+      float m = -INFINITY, l = 0.0f;
+      for (int i = 0; i < nkt; ++i) {
+        DA_TRACE(13 + t, i, tr);
+        mbar_wait(&bars[B_SFULL + t], i & 1);
+        DA_TRACE(3 * t, i, tr);
+        tc_fence_after();
+        uint32_t sr[BN];
+#pragma unroll
+        for (int c = 0; c < BN / 32; ++c) tmem_ld32(tS + 32u * c, *reinterpret_cast<uint32_t(*)[32]>(&sr[32 * c]));
+        tmem_ld_wait();
+#if DA_PINGPONG == 2
+        tc_fence_before();
+        mbar_arrive(&bars[B_SLD + t]);  // S_t(i) is in registers: the lower half of S_t(i+1) may land
+#endif
+        float sv[BN];
+#pragma unroll
+        for (int e = 0; e < BN; ++e) sv[e] = __uint_as_float(sr[e]);
+        const int kbase = i * BN;
+        if (kbase + BN > args.N || (args.causal && kbase + BN - 1 > q0)) {
+          const int lim = args.causal ? min(args.N - 1, q_row) : args.N - 1;
+#pragma unroll
+          for (int e = 0; e < BN; ++e)
+            if (kbase + e > lim) sv[e] = -INFINITY;
+        }
+        float mx8[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) mx8[j] = max3(sv[j], sv[8 + j], sv[120 + j]);
+#pragma unroll
+        for (int e = 16; e < 120; e += 16)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) mx8[j] = max3(mx8[j], sv[e + j], sv[e + 8 + j]);
+        const float mx = max3(max3(mx8[0], mx8[1], mx8[2]), max3(mx8[3], mx8[4], mx8[5]), fmaxf(mx8[6], mx8[7]));
+        const float mnew = fmaxf(m, mx * sl2);
+        DA_TRACE(3 * t + 1, i, tr);
+        if (i == 0) {
+          m = mnew;
+        } else {
+          const bool need = mnew > m + 8.0f;
+          if (__any_sync(0xffffffffu, need)) {
+            const float f = need ? ex2(m - mnew) : 1.0f;
+#pragma unroll 1
+            for (int c = 0; c < D / 16; ++c) {
+              uint32_t r[16];
+              tmem_ld16(tO + 16u * c, r);
+              tmem_ld_wait();
+#pragma unroll
+              for (int e = 0; e < 16; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * f);
+              tmem_st16(tO + 16u * c, r);
+            }
+            if (need) {
+              l *= f;
+              m = mnew;
+            }
+          }
+        }
+        const float2 sl2x2 = make_float2(sl2, sl2), nm2 = make_float2(-m, -m);
+        float2 acc[4] = {make_float2(0.f, 0.f), make_float2(0.f, 0.f), make_float2(0.f, 0.f),
+                         make_float2(0.f, 0.f)};
+        uint32_t pr[64];
+        constexpr uint32_t kPcol = DA_PINGPONG == 2 ? 64u : 0u;  // P_t columns inside S_t
+#if DA_EXP_SPLIT && DA_PV_SPLIT
+        // keys 0-63, then 64-127; in each half the MUFU pairs first, the polynomial pairs after
+#pragma unroll
+        for (int hh = 0; hh < 2; ++hh) {
+#pragma unroll
+          for (int pass = 0; pass < 2; ++pass) {
+#pragma unroll
+            for (int e = 32 * hh; e < 32 * hh + 32; ++e) {
+              const bool poly = (e & 7) >= 8 - EMU;
+              if (poly != (pass == 1)) continue;
+              const float2 x = fma2(make_float2(sv[2 * e], sv[2 * e + 1]), sl2x2, nm2);
+              const float2 p = poly ? exp2_poly2(x) : make_float2(ex2(x.x), ex2(x.y));
+              acc[e & 3] = fadd2(acc[e & 3], p);
+              pr[e] = pack_bf16x2(p.x, p.y);
+            }
+          }
+          tmem_st32(tS + kPcol + 32u * hh, *reinterpret_cast<uint32_t(*)[32]>(&pr[32 * hh]));
+          if (hh == 0) {
+            tmem_st_wait();
+            tc_fence_before();
+            mbar_arrive(&bars[B_PHALF + t]);
+          }
+        }
+#elif DA_EXP_SPLIT
+#pragma unroll
+        for (int pass = 0; pass < 2; ++pass) {
+#pragma unroll
+          for (int e = 0; e < 64; ++e) {
+            const bool poly = (e & 7) >= 8 - EMU;
+            if (poly != (pass == 1)) continue;
+            const float2 x = fma2(make_float2(sv[2 * e], sv[2 * e + 1]), sl2x2, nm2);
+            const float2 p = poly ? exp2_poly2(x) : make_float2(ex2(x.x), ex2(x.y));
+            acc[e & 3] = fadd2(acc[e & 3], p);
+            pr[e] = pack_bf16x2(p.x, p.y);
+          }
+        }
+#pragma unroll
+        for (int c = 0; c < 2; ++c) tmem_st32(tS + kPcol + 32u * c, *reinterpret_cast<uint32_t(*)[32]>(&pr[32 * c]));
+#else
+#pragma unroll
+        for (int e = 0; e < 64; ++e) {
+          const float2 x = fma2(make_float2(sv[2 * e], sv[2 * e + 1]), sl2x2, nm2);
+          float2 p;
+          if ((e & 7) >= 8 - EMU)
+            p = exp2_poly2(x);
+          else
+            p = make_float2(ex2(x.x), ex2(x.y));
+          acc[e & 3] = fadd2(acc[e & 3], p);
+          pr[e] = pack_bf16x2(p.x, p.y);
+          if ((e & 7) == 7) tmem_st8(tS + kPcol + (e - 7), &pr[e - 7]);
+        }
+#endif
+        DA_TRACE(16 + t, i, tr);
+        const float2 a = fadd2(fadd2(acc[0], acc[1]), fadd2(acc[2], acc[3]));
+        l += a.x + a.y;
+        tmem_st_wait();
+        tc_fence_before();
+        mbar_arrive(&bars[B_PFULL + t]);
+        DA_TRACE(3 * t + 2, i, tr);
+      }
+      if (nkt > 0) {
+        mbar_wait(&bars[B_OFULL + t], 0);
+        tc_fence_after();
+        const float inv = 1.0f / l;
+#pragma unroll
+        for (int c = 0; c < D / 32; ++c) {
+          uint32_t r[32];
+          tmem_ld32(tO + 32u * c, r);
+          tmem_ld_wait();
+          if (q_row < args.N) {
+            const size_t off = ((size_t)bh * args.N + q_row) * D + 32 * c;
+            if (args.out_f32) {
+              float4* o = reinterpret_cast<float4*>(static_cast<float*>(args.out) + off);
+#pragma unroll
+              for (int e = 0; e < 8; ++e)
+                o[e] = make_float4(__uint_as_float(r[4 * e]) * inv, __uint_as_float(r[4 * e + 1]) * inv,
+                                   __uint_as_float(r[4 * e + 2]) * inv, __uint_as_float(r[4 * e + 3]) * inv);
+            } else {
+              uint4* o = reinterpret_cast<uint4*>(static_cast<uint16_t*>(args.out) + off);
+#pragma unroll
+              for (int e = 0; e < 4; ++e)
+                o[e] = make_uint4(pack_bf16x2(__uint_as_float(r[8 * e]) * inv, __uint_as_float(r[8 * e + 1]) * inv),
+                                  pack_bf16x2(__uint_as_float(r[8 * e + 2]) * inv, __uint_as_float(r[8 * e + 3]) * inv),
+                                  pack_bf16x2(__uint_as_float(r[8 * e + 4]) * inv, __uint_as_float(r[8 * e + 5]) * inv),
+                                  pack_bf16x2(__uint_as_float(r[8 * e + 6]) * inv, __uint_as_float(r[8 * e + 7]) * inv));
+            }
+          }
+        }
+        if (args.lse && q_row < args.N)
+          args.lse[(size_t)bh * args.N + q_row] = (m + log2f(l)) * 0.69314718055994531f;
+      }
+    }
+  } else if (false) {
+#endif
     if constexpr (kSplit == 2) {
       if (DISTR) asm volatile("setmaxnreg.inc.sync.aligned.u32 160;");
     }
@@ -748,6 +1040,9 @@ __global__ void __launch_bounds__(threads_of<DISTR>(), 1)
         args.lse[(size_t)bh * args.N + q_row] = (m[t] + log2f(lt)) * 0.69314718055994531f;
     }
   } else {
+#if DA_PINGPONG
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 96;");
+#endif
     // ------------------------------------------------------------------ fusion (warps 12..15)
     // Thread f owns 16-byte chunk ch = f % 16 (8 keys) of K̂^T rows j = f/16 + 8n, n < DR/8.
     // Its source-row byte offsets (perm rows * 256 + ch * 16) are fixed for the CTA's lifetime,

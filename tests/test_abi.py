@@ -117,11 +117,11 @@ def test_status_strings(L):
 
 def test_backward_workspace_size_query_is_host_only(L):
     # fused path (d=128): perm [BH][nqb][d] + Q̃ [BH][N][d] bf16 + D, lse_pad [BH][N_pad128] fp32
-    # + dQ̃ [BH][N][d] fp32
+    # (dQ̃ is folded into dQ inside the dQ̃ kernel: no fp32 dQ̃ workspace)
     p = params(B=2, H=4, N=1000, d=128, block_l=128, G=2)
     al = lambda x: (x + 255) // 256 * 256
     BH, N, d, Np = 8, 1000, 128, 1024
-    want = al(BH * 8 * d) + al(BH * N * d * 2) + 2 * al(BH * Np * 4) + al(BH * N * d * 4)
+    want = al(BH * 8 * d) + al(BH * N * d * 2) + 2 * al(BH * Np * 4)
     assert L.distr_attn_bwd_workspace_size(ctypes.byref(p)) == want
     assert L.distr_attn_bwd_workspace_size(ctypes.byref(params(d=96))) == 0
     assert da.distr_attn_bwd_workspace_size((2, 4, 1000, 128), 4) == want
