@@ -835,12 +835,11 @@ int distr_attn_plan(int N, int d, int block_l, int group_size, int distr, da_pla
   return DA_OK;
 }
 
-// Cost-model constants (clk on one SM), measured on this build: the CTA prologue (distr: Q landed
-// + in-CTA hash + rank + Q̂ build + first S) from CTA-0 timelines (tools/calibrate.sh,
-// profiles/r02_v1/calib.txt); the steady clk per 128-key step of a CTA (two Q tiles) for d = 128
-// from the long-sequence sweeps (N = 32k / 64k, where the prologue is < 2 % of the time: the
-// distr/exact time ratios of profiles/r02_v1 and r02_v2, averaged, times the exact kernel's
-// timeline step); d = 64 steps from the timelines.
+// Cost-model constants (clk on one SM at the 1800 MHz reference clock). d = 128: the CTA prologue
+// (distr: Q landed + in-CTA hash + rank + Q̂ build + first S) and the steady clk per 128-key step
+// of a CTA (two Q tiles), least-squares fits (tools/fit_planner.py) to the C4 N sweep of the
+// ping-pong kernels (profiles/r02_v6/sweep*.json); d = 64 from the round-2 CTA timelines
+// (tools/calibrate.sh, profiles/r02_v1/calib.txt).
 struct StepCost {
   int d, l, G;
   double step, prologue;
@@ -848,10 +847,10 @@ struct StepCost {
 constexpr StepCost kDistrCost[] = {
     {64, 64, 2, 3169, 13342},  {64, 128, 2, 3100, 11030}, {64, 128, 4, 3190, 11367},
     {64, 256, 2, 3045, 14314}, {64, 256, 4, 3112, 16459}, {128, 64, 2, 4625, 27688},
-    {128, 128, 2, 3088, 19609}, {128, 128, 4, 3004, 19108}, {128, 256, 2, 3088, 23418},
-    {128, 256, 4, 2953, 22970},
+    {128, 128, 2, 3141, 14446}, {128, 128, 4, 3075, 18445}, {128, 256, 2, 3013, 15872},
+    {128, 256, 4, 2847, 19427},
 };
-constexpr double kExactStep64 = 3268, kExactStep128 = 3356, kExactPrologue = 6000;
+constexpr double kExactStep64 = 3268, kExactStep128 = 3349, kExactPrologue = 6000;
 
 // Predicted kernel time (us) of one flavour: CTAs (Q tile pairs) list-scheduled over 148 SMs.
 double predict_attn_us(int BH, int N, int causal, double step, double prologue, double mhz) {

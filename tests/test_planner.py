@@ -102,7 +102,8 @@ import json
 import os
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-PROFILE = sorted(glob.glob(os.path.join(ROOT, "profiles", "r02_v*")))[-1]
+PROFILE = sorted(p for p in glob.glob(os.path.join(ROOT, "profiles", "r02_v*"))
+                 if os.path.exists(os.path.join(p, "sweep.json")) and os.path.exists(os.path.join(p, "sweep_l256.json")))[-1]
 
 
 def measured():
